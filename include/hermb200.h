@@ -1,0 +1,190 @@
+/*
+ * hermb200 — C ABI of the B200-native Hermite wave-solver hot path.
+ *
+ * The reference package (`hermwave`, pure Python/numpy) has no FFI: its
+ * boundary is the Python functions re-exported in pkg/src/hermwave/__init__.py.
+ * Each entry point below replaces one of them; the Python mirror in
+ * paper_1802_05246_b200/ binds these symbols with ctypes.
+ *
+ * Conventions
+ *  - All field pointers are DEVICE pointers (FP64, C order), laid out exactly
+ *    like the reference's Field arrays:
+ *        2D  values[i][j][k][l]  (grid.py:113-116; k = x order, l = y order)
+ *        1D  values[i][l]        (grid.py:82-84)
+ *  - Every call is stream-ordered on `stream` (a cudaStream_t; NULL = legacy
+ *    default stream) and returns an int status: 0 ok, < 0 error.  The error
+ *    text is available from hw_last_error() (thread local).  No call throws.
+ *  - Scalars (dt, h, speed) are passed exactly as the reference computes them
+ *    (SchemeConfig.dt, Grid.h), so a caller reproduces the reference's
+ *    time bookkeeping on the host.
+ */
+#ifndef HERMB200_H
+#define HERMB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* boundary.py:24 KINDS */
+#define HW_PERIODIC   0
+#define HW_DIRICHLET0 1
+#define HW_NEUMANN0   2
+
+/* grid.py:19-20 PRIMAL / DUAL */
+#define HW_PRIMAL 0
+#define HW_DUAL   1
+
+#define HW_OK            0
+#define HW_EINVAL       -1
+#define HW_ECUDA        -2
+#define HW_EUNSUPPORTED -3
+
+/* One axis of BoundarySpec (boundary.py:29-47). */
+typedef struct {
+  int32_t left_kind, right_kind;
+  double left_value, right_value;
+} hw_axis_bc;
+
+/*
+ * Source-row view of a 2D field for one half step, with optional slab
+ * decomposition along x (axis 0).  Rows [row0, row0+nrows) are local and
+ * contiguous at `base`; `halo_lo` / `halo_hi` (may be NULL) hold global rows
+ * row0-1 / row0+nrows received from the neighbouring ranks.  On a single
+ * device: row0 = 0, nrows = nx, halos NULL.
+ */
+typedef struct {
+  const double* base;
+  const double* halo_lo;
+  const double* halo_hi;
+  int64_t row0, nrows;
+} hw_rows2d;
+
+/* Common 2D step geometry (grid.py:58-79, boundary.py:101-168). */
+typedef struct {
+  int64_t nx, ny;          /* GLOBAL source node counts of the source parity */
+  int32_t parity_src;      /* HW_PRIMAL / HW_DUAL */
+  int32_t periodic;        /* Grid2D.periodic */
+  hw_axis_bc bcx, bcy;     /* BoundarySpec2D.x / .y (values used for u only) */
+  int64_t trow0, ntrows;   /* target rows to produce (global index, count);
+                              ntrows < 0 => all target rows */
+} hw_geom2d;
+
+/* Library info. */
+const char* hw_last_error(void);
+int hw_version(void);
+int hw_max_order(void);            /* largest m with a compiled fast path */
+
+/* interp.py:51-75 interp_matrix(mu): (2mu+2)^2 row-major, exact doubles. */
+int hw_interp_matrix(int mu, double* out_host);
+
+/* Number of target nodes per axis produced from `n_src` source nodes. */
+int64_t hw_target_count(int64_t n_src, int parity_src, int periodic);
+
+/*
+ * dissipative.py:215-247 half_step_2d (stabilised 2D half step).
+ * u: orders (m,m), v: orders (m-1,m-1).  Writes target rows
+ * [trow0, trow0+ntrows) of the opposite parity into u_dst / v_dst
+ * (row trow0 at offset 0).  stage_cap <= 0 selects the default 4m+4.
+ */
+int hw_diss2d_half_step(const hw_rows2d* u_src, const hw_rows2d* v_src,
+                        double* u_dst, double* v_dst, int m,
+                        const hw_geom2d* geom, double dt, double hx, double hy,
+                        double speed, int stage_cap, void* stream);
+
+/*
+ * conservative.py:139-157 full_step_conservative (2D):
+ * out = 2 * WT . I_{m,m}(current) - previous.  `out` may alias `previous`.
+ */
+int hw_cons2d_step(const hw_rows2d* cur_src, const double* prev, double* out,
+                   int m, const hw_geom2d* geom, double dt, double hx, double hy,
+                   double speed, void* stream);
+
+/*
+ * conservative.py:166-195 bootstrap_first_half (2D): plain recursion on
+ * I_m g0 and I_m g1 (both order (m,m)), 4m+4 stages, evaluated at theta=1/2.
+ */
+int hw_boot2d(const hw_rows2d* g0_src, const hw_rows2d* g1_src, double* out,
+              int m, const hw_geom2d* geom, double dt, double hx, double hy,
+              double speed, void* stream);
+
+/*
+ * dissipative.py:160-181 half_step_1d.  forcing (may be NULL) is a device
+ * array F[s-1][l][t] (s = 1..stages, l < m, t < n_targets) of the already
+ * scaled terms h^l dt^s/(l! s!) f(l, s-1, x_t, time) (dissipative.py:102-105).
+ */
+int hw_diss1d_half_step(const double* u_src, const double* v_src,
+                        double* u_dst, double* v_dst, int m, int64_t n_src,
+                        int parity_src, const hw_axis_bc* bc, double dt,
+                        double h, double speed, int stages,
+                        const double* forcing, void* stream);
+
+/* conservative.py:139-157 full_step_conservative (1D).  out may alias prev. */
+int hw_cons1d_step(const double* cur, const double* prev, double* out, int m,
+                   int64_t n_src, int parity_src, const hw_axis_bc* bc,
+                   double lam, void* stream);
+
+/* conservative.py:166-184 bootstrap_first_half (1D), 2m+3 stages. */
+int hw_boot1d(const double* g0, const double* g1, double* out, int m,
+              int64_t n_src, int parity_src, const hw_axis_bc* bc, double dt,
+              double h, double speed, void* stream);
+
+/*
+ * diagnostics.py:118-135 l2_error_field_2d, reduced on the device.
+ * The field (orders (mx,my)) is interpolated on every target cell of its own
+ * corner gather and evaluated at npts^2 Gauss points; `exact` is either a
+ * device array exact[ci][cj][p][q] (exact_kind = 0) or one of the built-in
+ * closed forms (exact_kind = 1 plane wave sin(w(x+y+sqrt2 t)), params =
+ * {w, t}; exact_kind = 2 standing wave sin(kx x) sin(ky y) cos(om t),
+ * params = {kx, ky, om, t}).  Node coordinates: x_left/y_left, hx/hy.
+ * Result (the sum before sqrt, i.e. the squared error) is written to
+ * *out_host after a stream synchronisation.
+ */
+int hw_l2err2d(const hw_rows2d* src, int mx, int my, const hw_geom2d* geom,
+               double x_left, double y_left, double hx, double hy, int npts,
+               const double* gauss_x, const double* gauss_w,
+               int exact_kind, const double* exact, const double* params,
+               double* out_host, void* stream);
+
+/*
+ * diagnostics.py:66-115 per-piece 1D L2 errors.  For each target piece t the
+ * caller supplies the clipped Gauss abscissae in the piece's scaled variable
+ * (xi[t][p]), the weights times half-width (w[t][p]) and the exact values
+ * ex[t][p]; deriv selects the field (0) or its first derivative (1, scaled
+ * by 1/h like CellPolynomial.derivative).  Squared error -> *out_host.
+ */
+int hw_l2err1d(const double* src, int mu, int64_t n_src, int parity_src,
+               const hw_axis_bc* bc, double h, int deriv, int npts,
+               const double* xi, const double* w, const double* ex,
+               double* out_host, void* stream);
+
+/* driver.py:259-262 _require_finite: *nonfinite_host = count of non-finite. */
+int hw_count_nonfinite(const double* a, int64_t n, int64_t* nonfinite_host,
+                       void* stream);
+
+/*
+ * driver.py:241-256 planewave_data on the device: out[i][j][k][l] scaled
+ * blocks of sin(w(x+y+sqrt2 t)) (tder = 0) or its time derivative (tder = 1)
+ * at nodes x_i = x0 + hx*(i+off), y_j = y0 + hy*(j+off).
+ */
+int hw_init_planewave2d(double* out, int64_t nx, int64_t ny, int kx, int ky,
+                        double x0, double y0, double off, double t,
+                        double kappa, double hx, double hy, int tder,
+                        void* stream);
+
+/*
+ * Standing wave u = sin(ax x) sin(ay y) cos(om t) (tder = 0) or u_t
+ * (tder = 1) as scaled blocks; with trig shift phases (px, py) so that
+ * sin(pi x)cos(pi y) style products are expressible: sin(ax x + px) ...
+ */
+int hw_init_standing2d(double* out, int64_t nx, int64_t ny, int kx, int ky,
+                       double x0, double y0, double off, double t, double ax,
+                       double ay, double px, double py, double om, double hx,
+                       double hy, int tder, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HERMB200_H */

@@ -1,0 +1,681 @@
+// extern "C" boundary (include/hermb200.h): argument checking, constant-table
+// construction and kernel dispatch.  Never throws across the ABI.
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+#include "diag.cuh"
+#include "diss2d.cuh"
+#include "line1d.cuh"
+#include "tables.h"
+#include "taps2d.cuh"
+
+namespace hw {
+
+static thread_local std::string g_err;
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& s) : std::runtime_error(s), code(c) {}
+};
+
+#define HW_CHECK(cond, msg) \
+  do {                      \
+    if (!(cond)) throw Error(HW_EINVAL, msg); \
+  } while (0)
+
+static void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Error(HW_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+static int guard(F&& f) {
+  try {
+    f();
+    return HW_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HW_EINVAL;
+  }
+}
+
+static Rows to_rows(const hw_rows2d* r) {
+  Rows o;
+  o.base = r->base;
+  o.lo = r->halo_lo;
+  o.hi = r->halo_hi;
+  o.row0 = r->row0;
+  o.nrows = r->nrows;
+  return o;
+}
+
+static void check_bc_axis(const hw_axis_bc& b, int periodic) {
+  auto ok = [](int k) { return k == HW_PERIODIC || k == HW_DIRICHLET0 || k == HW_NEUMANN0; };
+  HW_CHECK(ok(b.left_kind) && ok(b.right_kind), "unknown boundary kind");
+  HW_CHECK((b.left_kind == HW_PERIODIC) == (b.right_kind == HW_PERIODIC),
+           "periodic must be specified on both opposing sides");
+  HW_CHECK((b.left_kind == HW_PERIODIC) == (periodic != 0),
+           "boundary spec and grid disagree about periodicity");
+}
+
+// phi(a) = a! r^floor(a/2) (dissipative / bootstrap) or a! r^a (conservative)
+static std::vector<double> phi_table(int n, double r, bool full_power) {
+  std::vector<double> p(n);
+  for (int a = 0; a < n; ++a) {
+    const int e = full_power ? a : a / 2;
+    double rp = 1.0;
+    for (int q = 0; q < e; ++q) rp *= r;
+    p[a] = factorial(a) * rp;
+  }
+  return p;
+}
+
+// ------------------------------------------------------------------ diss2d
+template <int M>
+static void launch_diss2d(const Step2DArgs& a, double dt, double rx, double ry, int S, cudaStream_t st) {
+  Diss2DParams<M> P;
+  P.a = a;
+  auto& T = P.t;
+  const std::vector<double> hm = hermite_left_block(M);
+  const std::vector<double> hm1 = hermite_left_block(M - 1);
+  const std::vector<double> px = phi_table(2 * M + 2, rx, false);
+  const std::vector<double> py = phi_table(2 * M + 2, ry, false);
+  for (int a2 = 0; a2 < 2 * M + 2; ++a2)
+    for (int k = 0; k <= M; ++k) {
+      T.mx[a2][k] = px[a2] * hm[a2 * (M + 1) + k];
+      T.my[a2][k] = py[a2] * hm[a2 * (M + 1) + k];
+    }
+  for (int a2 = 0; a2 < 2 * M; ++a2)
+    for (int k = 0; k < M; ++k) {
+      T.mx1[a2][k] = px[a2] * hm1[a2 * M + k];
+      T.my1[a2][k] = py[a2] * hm1[a2 * M + k];
+    }
+  const double th = 0.5;
+  for (int i = 0; i < M; ++i)
+    for (int j = 0; j < M; ++j) {
+      const int p = i + j;
+      const double c = binom(p, i);
+      auto pw = [](double x, int e) {
+        double r = 1.0;
+        for (int q = 0; q < e; ++q) r *= x;
+        return r;
+      };
+      T.gA[i][j] = (2 * p + 1 <= S) ? c * pw(th, 2 * p + 1) * pw(dt, p + 1) / factorial(2 * p + 1) : 0.0;
+      T.gB[i][j] = (2 * p + 2 <= S) ? c * pw(th, 2 * p + 2) * pw(dt, p + 1) / factorial(2 * p + 2) : 0.0;
+      T.gG[i][j] = (2 * p <= S) ? c * pw(th, 2 * p) * pw(dt, p) / factorial(2 * p) : 0.0;
+      T.gD[i][j] = (2 * p + 1 <= S) ? c * pw(th, 2 * p + 1) * pw(dt, p) / factorial(2 * p + 1) : 0.0;
+    }
+  for (int k = 0; k <= M; ++k)
+    for (int l = 0; l <= M; ++l) T.inv[k][l] = 1.0 / (px[k] * py[l]);
+
+  using S_ = Diss2DSmem<M>;
+  const int smem = S_::bytes + kTileJ * (S_::PU + S_::PV) * 8;
+  cuda_check(cudaFuncSetAttribute(diss2d_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+             "cudaFuncSetAttribute(diss2d)");
+  const int64_t nct = (a.nty + kTileJ - 1) / kTileJ;
+  const int64_t gy = a.ntrows < 65535 ? a.ntrows : 65535;
+  dim3 grid((unsigned)nct, (unsigned)gy);
+  diss2d_kernel<M><<<grid, 128, smem, st>>>(P);
+  cuda_check(cudaGetLastError(), "diss2d launch");
+}
+
+// ------------------------------------------------------------------ taps2d
+template <int M, int NIN>
+static void launch_taps2d(const Taps2DArgs& a, const std::vector<double>& px, const std::vector<double>& py,
+                          const std::vector<std::vector<double>>& g, double scale, cudaStream_t st) {
+  Taps2DParams<M, NIN> P;
+  P.a = a;
+  auto& T = P.t;
+  const std::vector<double> hm = hermite_left_block(M);
+  for (int a2 = 0; a2 < 2 * M + 2; ++a2)
+    for (int k = 0; k <= M; ++k) {
+      T.mx[a2][k] = px[a2] * hm[a2 * (M + 1) + k];
+      T.my[a2][k] = py[a2] * hm[a2 * (M + 1) + k];
+    }
+  for (int f = 0; f < NIN; ++f)
+    for (int i = 0; i <= M; ++i)
+      for (int j = 0; j <= M; ++j) T.g[f][i][j] = g[f][i * (M + 1) + j];
+  for (int k = 0; k <= M; ++k)
+    for (int l = 0; l <= M; ++l) T.inv[k][l] = scale / (px[k] * py[l]);
+  using S_ = Taps2DSmem<M>;
+  const int smem = (NIN * 2 * S_::NQ * S_::PP + kTileJ * S_::P) * 8;
+  cuda_check(cudaFuncSetAttribute(taps2d_kernel<M, NIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+             "cudaFuncSetAttribute(taps2d)");
+  const int64_t nct = (a.nty + kTileJ - 1) / kTileJ;
+  const int64_t gy = a.ntrows < 65535 ? a.ntrows : 65535;
+  dim3 grid((unsigned)nct, (unsigned)gy);
+  taps2d_kernel<M, NIN><<<grid, 128, smem, st>>>(P);
+  cuda_check(cudaGetLastError(), "taps2d launch");
+}
+
+template <template <int> class F, class... A>
+static void dispatch_m(int m, A&&... args) {
+  switch (m) {
+    case 1: F<1>::run(args...); break;
+    case 2: F<2>::run(args...); break;
+    case 3: F<3>::run(args...); break;
+    case 4: F<4>::run(args...); break;
+    case 5: F<5>::run(args...); break;
+    case 6: F<6>::run(args...); break;
+    case 7: F<7>::run(args...); break;
+    case 8: F<8>::run(args...); break;
+    default: throw Error(HW_EUNSUPPORTED, "method order m=" + std::to_string(m) + " has no compiled 2D path (1..8)");
+  }
+}
+
+template <int M>
+struct Diss2DRun {
+  static void run(const Step2DArgs& a, double dt, double rx, double ry, int S, cudaStream_t st) {
+    launch_diss2d<M>(a, dt, rx, ry, S, st);
+  }
+};
+template <int M>
+struct ConsRun {
+  static void run(const Taps2DArgs& a, const std::vector<double>& px, const std::vector<double>& py,
+                  const std::vector<std::vector<double>>& g, double scale, cudaStream_t st) {
+    launch_taps2d<M, 1>(a, px, py, g, scale, st);
+  }
+};
+template <int M>
+struct BootRun {
+  static void run(const Taps2DArgs& a, const std::vector<double>& px, const std::vector<double>& py,
+                  const std::vector<std::vector<double>>& g, double scale, cudaStream_t st) {
+    launch_taps2d<M, 2>(a, px, py, g, scale, st);
+  }
+};
+
+struct Geo {
+  int64_t nx, ny, ntx, nty, trow0, ntrows;
+  int off, periodic;
+};
+
+static Geo check_geom(const hw_geom2d* g) {
+  HW_CHECK(g, "null geometry");
+  HW_CHECK(g->nx >= 1 && g->ny >= 1, "need at least one source node per axis");
+  HW_CHECK(g->parity_src == HW_PRIMAL || g->parity_src == HW_DUAL, "unknown parity");
+  check_bc_axis(g->bcx, g->periodic);
+  check_bc_axis(g->bcy, g->periodic);
+  Geo o;
+  o.nx = g->nx;
+  o.ny = g->ny;
+  o.periodic = g->periodic != 0;
+  o.off = src_offset(g->parity_src);
+  o.ntx = target_count(g->nx, g->parity_src, o.periodic);
+  o.nty = target_count(g->ny, g->parity_src, o.periodic);
+  HW_CHECK(o.ntx >= 1 && o.nty >= 1, "grid too small for a half step");
+  o.trow0 = g->trow0;
+  o.ntrows = g->ntrows < 0 ? o.ntx - g->trow0 : g->ntrows;
+  HW_CHECK(o.trow0 >= 0 && o.trow0 + o.ntrows <= o.ntx, "target row range out of bounds");
+  return o;
+}
+
+}  // namespace hw
+
+using namespace hw;
+
+extern "C" {
+
+const char* hw_last_error(void) { return g_err.c_str(); }
+int hw_version(void) { return 1; }
+int hw_max_order(void) { return kMaxFast; }
+
+int hw_interp_matrix(int mu, double* out) {
+  return guard([&] {
+    HW_CHECK(out, "null output");
+    HW_CHECK(mu >= 0 && mu <= kMaxOrder, "interpolation order must be in [0, 12]");
+    const std::vector<double> m = hermite_matrix(mu);
+    std::memcpy(out, m.data(), m.size() * sizeof(double));
+  });
+}
+
+int64_t hw_target_count(int64_t n_src, int parity_src, int periodic) {
+  return target_count(n_src, parity_src, periodic);
+}
+
+int hw_diss2d_half_step(const hw_rows2d* u_src, const hw_rows2d* v_src, double* u_dst, double* v_dst, int m,
+                        const hw_geom2d* geom, double dt, double hx, double hy, double speed, int stage_cap,
+                        void* stream) {
+  return guard([&] {
+    HW_CHECK(u_src && v_src && u_src->base && v_src->base && u_dst && v_dst, "null field pointer");
+    HW_CHECK(m >= 1, "method order must be >= 1");
+    const Geo g = check_geom(geom);
+    if (g.ntrows == 0) return;
+    Step2DArgs a;
+    a.u = to_rows(u_src);
+    a.v = to_rows(v_src);
+    a.ud = u_dst;
+    a.vd = v_dst;
+    a.nx = g.nx;
+    a.ny = g.ny;
+    a.trow0 = g.trow0;
+    a.ntrows = g.ntrows;
+    a.nty = g.nty;
+    a.off = g.off;
+    a.periodic = g.periodic;
+    a.kxl = g.periodic ? 0 : geom->bcx.left_kind;
+    a.kxh = g.periodic ? 0 : geom->bcx.right_kind;
+    a.kyl = g.periodic ? 0 : geom->bcy.left_kind;
+    a.kyh = g.periodic ? 0 : geom->bcy.right_kind;
+    a.gxl = geom->bcx.left_value;
+    a.gxh = geom->bcx.right_value;
+    a.gyl = geom->bcy.left_value;
+    a.gyh = geom->bcy.right_value;
+    // dissipative.py:227,234-235 (rx, ry exactly as the reference forms them)
+    const double rx = speed * speed * dt / (hx * hx);
+    const double ry = speed * speed * dt / (hy * hy);
+    const int S = stage_cap > 0 ? stage_cap : 4 * m + 4;
+    dispatch_m<Diss2DRun>(m, a, dt, rx, ry, S, (cudaStream_t)stream);
+  });
+}
+
+static Taps2DArgs taps_args(const Geo& g, const hw_geom2d* geom, const hw_rows2d* f0, const hw_rows2d* f1,
+                            const double* prev, double* out) {
+  Taps2DArgs a;
+  a.f0 = to_rows(f0);
+  a.f1 = f1 ? to_rows(f1) : a.f0;
+  a.prev = prev;
+  a.out = out;
+  a.nx = g.nx;
+  a.ny = g.ny;
+  a.trow0 = g.trow0;
+  a.ntrows = g.ntrows;
+  a.nty = g.nty;
+  a.off = g.off;
+  a.periodic = g.periodic;
+  a.kxl = g.periodic ? 0 : geom->bcx.left_kind;
+  a.kxh = g.periodic ? 0 : geom->bcx.right_kind;
+  a.kyl = g.periodic ? 0 : geom->bcy.left_kind;
+  a.kyh = g.periodic ? 0 : geom->bcy.right_kind;
+  a.gxl = geom->bcx.left_value;
+  a.gxh = geom->bcx.right_value;
+  a.gyl = geom->bcy.left_value;
+  a.gyh = geom->bcy.right_value;
+  a.g1scale = 0.0;
+  return a;
+}
+
+int hw_cons2d_step(const hw_rows2d* cur_src, const double* prev, double* out, int m, const hw_geom2d* geom,
+                   double dt, double hx, double hy, double speed, void* stream) {
+  return guard([&] {
+    HW_CHECK(cur_src && cur_src->base && prev && out, "null field pointer");
+    HW_CHECK(m >= 1, "method order must be >= 1");
+    const Geo g = check_geom(geom);
+    if (g.ntrows == 0) return;
+    Taps2DArgs a = taps_args(g, geom, cur_src, nullptr, prev, out);
+    // conservative.py:133-136: rho = c dt / (2h) per axis
+    const double rhox = 0.5 * speed * dt / hx, rhoy = 0.5 * speed * dt / hy;
+    const int K = 2 * m + 2;
+    std::vector<double> px = phi_table(K, rhox, true), py = phi_table(K, rhoy, true);
+    std::vector<std::vector<double>> gt(1, std::vector<double>((size_t)(m + 1) * (m + 1)));
+    for (int i = 0; i <= m; ++i)
+      for (int j = 0; j <= m; ++j) gt[0][i * (m + 1) + j] = binom(i + j, i) / factorial(2 * i + 2 * j);
+    dispatch_m<ConsRun>(m, a, px, py, gt, 2.0, (cudaStream_t)stream);
+  });
+}
+
+int hw_boot2d(const hw_rows2d* g0_src, const hw_rows2d* g1_src, double* out, int m, const hw_geom2d* geom,
+              double dt, double hx, double hy, double speed, void* stream) {
+  return guard([&] {
+    HW_CHECK(g0_src && g1_src && g0_src->base && g1_src->base && out, "null field pointer");
+    HW_CHECK(m >= 1, "method order must be >= 1");
+    const Geo g = check_geom(geom);
+    if (g.ntrows == 0) return;
+    Taps2DArgs a = taps_args(g, geom, g0_src, g1_src, nullptr, out);
+    const double rx = speed * speed * dt / (hx * hx), ry = speed * speed * dt / (hy * hy);
+    const int K = 2 * m + 2;
+    std::vector<double> px = phi_table(K, rx, false), py = phi_table(K, ry, false);
+    std::vector<std::vector<double>> gt(2, std::vector<double>((size_t)(m + 1) * (m + 1)));
+    const double th = 0.5;
+    const int S = 4 * m + 4;  // conservative.py:192
+    for (int i = 0; i <= m; ++i)
+      for (int j = 0; j <= m; ++j) {
+        const int p = i + j;
+        double thp = 1.0, dtp = 1.0;
+        for (int q = 0; q < 2 * p; ++q) thp *= th;
+        for (int q = 0; q < p; ++q) dtp *= dt;
+        gt[0][i * (m + 1) + j] = (2 * p <= S) ? binom(p, i) * thp * dtp / factorial(2 * p) : 0.0;
+        gt[1][i * (m + 1) + j] = (2 * p + 1 <= S) ? binom(p, i) * thp * th * dtp * dt / factorial(2 * p + 1) : 0.0;
+      }
+    dispatch_m<BootRun>(m, a, px, py, gt, 1.0, (cudaStream_t)stream);
+  });
+}
+
+// ------------------------------------------------------------------ 1D
+static std::unordered_map<int, double*>& hl_cache() {
+  static std::unordered_map<int, double*> c;
+  return c;
+}
+static std::mutex g_hl_mu;
+
+static const double* device_hl(int mu) {
+  std::lock_guard<std::mutex> lk(g_hl_mu);
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  const int key = dev * 64 + mu;
+  auto it = hl_cache().find(key);
+  if (it != hl_cache().end()) return it->second;
+  const std::vector<double> h = hermite_left_block(mu);
+  double* d = nullptr;
+  cuda_check(cudaMalloc(&d, h.size() * sizeof(double)), "cudaMalloc(hl)");
+  cuda_check(cudaMemcpy(d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice), "cudaMemcpy(hl)");
+  hl_cache()[key] = d;
+  return d;
+}
+
+static Line1DArgs line_args(int m, int64_t n_src, int parity_src, const hw_axis_bc* bc) {
+  HW_CHECK(bc, "null boundary spec");
+  HW_CHECK(m >= 1 && m <= kMax1D, "1D method order must be in [1, 12]");
+  const int periodic = bc->left_kind == HW_PERIODIC;
+  check_bc_axis(*bc, periodic);
+  HW_CHECK(parity_src == HW_PRIMAL || parity_src == HW_DUAL, "unknown parity");
+  Line1DArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.n = n_src;
+  a.nt = target_count(n_src, parity_src, periodic);
+  HW_CHECK(n_src >= 1 && a.nt >= 1, "grid too small for a half step");
+  a.off = src_offset(parity_src);
+  a.periodic = periodic;
+  a.kl = periodic ? 0 : bc->left_kind;
+  a.kh = periodic ? 0 : bc->right_kind;
+  a.gl = bc->left_value;
+  a.gh = bc->right_value;
+  a.m = m;
+  return a;
+}
+
+int hw_diss1d_half_step(const double* u_src, const double* v_src, double* u_dst, double* v_dst, int m,
+                        int64_t n_src, int parity_src, const hw_axis_bc* bc, double dt, double h, double speed,
+                        int stages, const double* forcing, void* stream) {
+  return guard([&] {
+    HW_CHECK(u_src && v_src && u_dst && v_dst, "null field pointer");
+    Line1DArgs a = line_args(m, n_src, parity_src, bc);
+    HW_CHECK(stages >= 1 && stages <= 4 * kMax1D, "stage count out of range");
+    a.u = u_src;
+    a.v = v_src;
+    a.ou = u_dst;
+    a.ov = v_dst;
+    a.forcing = forcing;
+    a.stages = stages;
+    a.dt = dt;
+    a.h = h;
+    a.speed = speed;
+    a.hl_u = device_hl(m);
+    a.hl_v = device_hl(m - 1);
+    const int thr = 128;
+    diss1d_kernel<<<(unsigned)((a.nt + thr - 1) / thr), thr, 0, (cudaStream_t)stream>>>(a);
+    cuda_check(cudaGetLastError(), "diss1d launch");
+  });
+}
+
+int hw_cons1d_step(const double* cur, const double* prev, double* out, int m, int64_t n_src, int parity_src,
+                   const hw_axis_bc* bc, double lam, void* stream) {
+  return guard([&] {
+    HW_CHECK(cur && prev && out, "null field pointer");
+    Line1DArgs a = line_args(m, n_src, parity_src, bc);
+    a.u = cur;
+    a.prev = prev;
+    a.ou = out;
+    a.rho = 0.5 * lam;  // conservative.py:125
+    a.hl_u = device_hl(m);
+    const int thr = 128;
+    cons1d_kernel<<<(unsigned)((a.nt + thr - 1) / thr), thr, 0, (cudaStream_t)stream>>>(a);
+    cuda_check(cudaGetLastError(), "cons1d launch");
+  });
+}
+
+int hw_boot1d(const double* g0, const double* g1, double* out, int m, int64_t n_src, int parity_src,
+              const hw_axis_bc* bc, double dt, double h, double speed, void* stream) {
+  return guard([&] {
+    HW_CHECK(g0 && g1 && out, "null field pointer");
+    Line1DArgs a = line_args(m, n_src, parity_src, bc);
+    a.u = g0;
+    a.v = g1;
+    a.ou = out;
+    a.stages = 2 * m + 3;  // conservative.py:183-184
+    a.dt = dt;
+    a.h = h;
+    a.speed = speed;
+    a.hl_u = device_hl(m);
+    const int thr = 128;
+    boot1d_kernel<<<(unsigned)((a.nt + thr - 1) / thr), thr, 0, (cudaStream_t)stream>>>(a);
+    cuda_check(cudaGetLastError(), "boot1d launch");
+  });
+}
+
+// ------------------------------------------------------------------ diagnostics
+struct DevBuf {
+  double* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+static double reduce_partials(double* part, int64_t n, cudaStream_t st) {
+  DevBuf out;
+  cuda_check(cudaMallocAsync(&out.p, sizeof(double), st), "cudaMallocAsync");
+  sum_partials_kernel<<<1, kRedThreads, 0, st>>>(part, n, out.p);
+  cuda_check(cudaGetLastError(), "sum_partials launch");
+  double h = 0.0;
+  cuda_check(cudaMemcpyAsync(&h, out.p, sizeof(double), cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+  cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+  cudaFreeAsync(out.p, st);
+  out.p = nullptr;
+  return h;
+}
+
+int hw_l2err2d(const hw_rows2d* src, int mx, int my, const hw_geom2d* geom, double x_left, double y_left,
+               double hx, double hy, int npts, const double* gauss_x, const double* gauss_w, int exact_kind,
+               const double* exact, const double* params, double* out_host, void* stream) {
+  return guard([&] {
+    HW_CHECK(src && src->base && gauss_x && gauss_w && out_host, "null pointer");
+    HW_CHECK(mx >= 0 && my >= 0 && mx <= kMaxOrder && my <= kMaxOrder, "orders out of range");
+    HW_CHECK(npts >= 1 && npts <= 64, "npts out of range");
+    HW_CHECK(exact_kind >= 0 && exact_kind <= 2, "unknown exact kind");
+    HW_CHECK(exact_kind != 0 || exact, "null exact array");
+    const Geo g = check_geom(geom);
+    cudaStream_t st = (cudaStream_t)stream;
+    // Ex[p][e] = sum_a (xg_p/2)^a M[a][e]   (diagnostics.py:128-130)
+    std::vector<double> gx(npts), gw(npts);
+    cuda_check(cudaMemcpy(gx.data(), gauss_x, npts * sizeof(double), cudaMemcpyDefault), "copy gauss x");
+    cuda_check(cudaMemcpy(gw.data(), gauss_w, npts * sizeof(double), cudaMemcpyDefault), "copy gauss w");
+    auto emat = [&](int mu) {
+      const std::vector<double> M = hermite_matrix(mu);
+      const int n = 2 * mu + 2;
+      std::vector<double> e((size_t)npts * n, 0.0);
+      for (int p = 0; p < npts; ++p) {
+        const double xi = 0.5 * gx[p];
+        for (int c = 0; c < n; ++c) {
+          double s = 0.0, pw = 1.0;
+          for (int a2 = 0; a2 < n; ++a2) {
+            s += pw * M[(size_t)a2 * n + c];
+            pw *= xi;
+          }
+          e[(size_t)p * n + c] = s;
+        }
+      }
+      return e;
+    };
+    const std::vector<double> ex = emat(mx), ey = emat(my);
+    const int64_t ncell = g.ntx * g.nty;
+    const int64_t nblk = (ncell + kRedThreads - 1) / kRedThreads;
+    DevBuf dex, dey, dgx, dgw, dpart;
+    cuda_check(cudaMalloc(&dex.p, ex.size() * 8), "cudaMalloc");
+    cuda_check(cudaMalloc(&dey.p, ey.size() * 8), "cudaMalloc");
+    cuda_check(cudaMalloc(&dgx.p, npts * 8), "cudaMalloc");
+    cuda_check(cudaMalloc(&dgw.p, npts * 8), "cudaMalloc");
+    cuda_check(cudaMalloc(&dpart.p, nblk * 8), "cudaMalloc");
+    cuda_check(cudaMemcpy(dex.p, ex.data(), ex.size() * 8, cudaMemcpyHostToDevice), "cudaMemcpy");
+    cuda_check(cudaMemcpy(dey.p, ey.data(), ey.size() * 8, cudaMemcpyHostToDevice), "cudaMemcpy");
+    cuda_check(cudaMemcpy(dgx.p, gx.data(), npts * 8, cudaMemcpyHostToDevice), "cudaMemcpy");
+    cuda_check(cudaMemcpy(dgw.p, gw.data(), npts * 8, cudaMemcpyHostToDevice), "cudaMemcpy");
+    L2Err2DArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.f = to_rows(src);
+    a.nx = g.nx;
+    a.ny = g.ny;
+    a.ntx = g.ntx;
+    a.nty = g.nty;
+    a.off = g.off;
+    a.periodic = g.periodic;
+    a.kxl = g.periodic ? 0 : geom->bcx.left_kind;
+    a.kxh = g.periodic ? 0 : geom->bcx.right_kind;
+    a.kyl = g.periodic ? 0 : geom->bcy.left_kind;
+    a.kyh = g.periodic ? 0 : geom->bcy.right_kind;
+    a.gxl = geom->bcx.left_value;
+    a.gxh = geom->bcx.right_value;
+    a.gyl = geom->bcy.left_value;
+    a.gyh = geom->bcy.right_value;
+    a.mx = mx;
+    a.my = my;
+    a.npts = npts;
+    a.ex = dex.p;
+    a.ey = dey.p;
+    a.gw = dgw.p;
+    a.gx = dgx.p;
+    a.exact_kind = exact_kind;
+    a.exact = exact;
+    for (int q = 0; q < 4; ++q) a.prm[q] = params ? params[q] : 0.0;
+    a.x0 = x_left;
+    a.y0 = y_left;
+    a.hx = hx;
+    a.hy = hy;
+    a.coff = geom->parity_src == HW_PRIMAL ? 0.5 : 0.0;  // targets live on the flipped parity
+    a.part = dpart.p;
+    l2err2d_kernel<<<(unsigned)nblk, kRedThreads, 0, st>>>(a);
+    cuda_check(cudaGetLastError(), "l2err2d launch");
+    const double s = reduce_partials(dpart.p, nblk, st);
+    *out_host = s * (0.25 * hx * hy);
+  });
+}
+
+int hw_l2err1d(const double* src, int mu, int64_t n_src, int parity_src, const hw_axis_bc* bc, double h, int deriv,
+               int npts, const double* xi, const double* w, const double* ex, double* out_host, void* stream) {
+  return guard([&] {
+    HW_CHECK(src && xi && w && ex && out_host, "null pointer");
+    HW_CHECK(mu >= 0 && mu <= kMaxOrder, "order out of range");
+    HW_CHECK(bc, "null boundary spec");
+    const int periodic = bc->left_kind == HW_PERIODIC;
+    check_bc_axis(*bc, periodic);
+    cudaStream_t st = (cudaStream_t)stream;
+    L2Err1DArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.f = src;
+    a.n = n_src;
+    a.nt = target_count(n_src, parity_src, periodic);
+    a.off = src_offset(parity_src);
+    a.periodic = periodic;
+    a.kl = periodic ? 0 : bc->left_kind;
+    a.kh = periodic ? 0 : bc->right_kind;
+    a.gl = bc->left_value;
+    a.gh = bc->right_value;
+    a.mu = mu;
+    a.deriv = deriv;
+    a.npts = npts;
+    a.h = h;
+    a.hl = device_hl(mu);
+    a.xi = xi;
+    a.w = w;
+    a.ex = ex;
+    const int64_t nblk = (a.nt + kRedThreads - 1) / kRedThreads;
+    DevBuf part;
+    cuda_check(cudaMalloc(&part.p, nblk * 8), "cudaMalloc");
+    a.part = part.p;
+    l2err1d_kernel<<<(unsigned)nblk, kRedThreads, 0, st>>>(a);
+    cuda_check(cudaGetLastError(), "l2err1d launch");
+    *out_host = reduce_partials(part.p, nblk, st);
+  });
+}
+
+int hw_count_nonfinite(const double* x, int64_t n, int64_t* out_host, void* stream) {
+  return guard([&] {
+    HW_CHECK(out_host, "null output");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n == 0) {
+      *out_host = 0;
+      return;
+    }
+    HW_CHECK(x, "null pointer");
+    unsigned long long* d = nullptr;
+    cuda_check(cudaMallocAsync((void**)&d, 8, st), "cudaMallocAsync");
+    cuda_check(cudaMemsetAsync(d, 0, 8, st), "cudaMemsetAsync");
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    nonfinite_kernel<<<(unsigned)blocks, 256, 0, st>>>(x, n, d);
+    cuda_check(cudaGetLastError(), "nonfinite launch");
+    unsigned long long h = 0;
+    cuda_check(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+    cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    cudaFreeAsync(d, st);
+    *out_host = (int64_t)h;
+  });
+}
+
+static void launch_init(const Init2DArgs& a, cudaStream_t st) {
+  const int64_t n = a.nx * a.ny;
+  if (n == 0) return;
+  init2d_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(a);
+  cuda_check(cudaGetLastError(), "init2d launch");
+}
+
+int hw_init_planewave2d(double* out, int64_t nx, int64_t ny, int kx, int ky, double x0, double y0, double off,
+                        double t, double kappa, double hx, double hy, int tder, void* stream) {
+  return guard([&] {
+    HW_CHECK(out, "null output");
+    Init2DArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.out = out;
+    a.nx = nx;
+    a.ny = ny;
+    a.kx = kx;
+    a.ky = ky;
+    a.x0 = x0;
+    a.y0 = y0;
+    a.off = off;
+    a.t = t;
+    a.hx = hx;
+    a.hy = hy;
+    a.kind = 1;
+    a.w = 2.0 * 3.141592653589793 * kappa;
+    a.tder = tder;
+    launch_init(a, (cudaStream_t)stream);
+  });
+}
+
+int hw_init_standing2d(double* out, int64_t nx, int64_t ny, int kx, int ky, double x0, double y0, double off,
+                       double t, double ax, double ay, double px, double py, double om, double hx, double hy,
+                       int tder, void* stream) {
+  return guard([&] {
+    HW_CHECK(out, "null output");
+    Init2DArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.out = out;
+    a.nx = nx;
+    a.ny = ny;
+    a.kx = kx;
+    a.ky = ky;
+    a.x0 = x0;
+    a.y0 = y0;
+    a.off = off;
+    a.t = t;
+    a.hx = hx;
+    a.hy = hy;
+    a.kind = 2;
+    a.ax = ax;
+    a.ay = ay;
+    a.px = px;
+    a.py = py;
+    a.om = om;
+    a.tder = tder;
+    launch_init(a, (cudaStream_t)stream);
+  });
+}
+
+}  // extern "C"

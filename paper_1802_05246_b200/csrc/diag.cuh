@@ -1,0 +1,235 @@
+// Diagnostics on the device: 2D / 1D L2 error reductions, the finite check
+// and the closed-form initial data generators.
+#pragma once
+
+#include "common.cuh"
+
+namespace hw {
+
+constexpr int kRedThreads = 256;
+
+// Deterministic block reduction (fixed tree order).
+__device__ inline double block_sum(double v, double* sh) {
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  const double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void sum_partials_kernel(const double* part, int64_t n, double* out) {
+  __shared__ double sh[kRedThreads];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+  const double r = block_sum(s, sh);
+  if (threadIdx.x == 0) *out = r;
+}
+
+struct L2Err2DArgs {
+  Rows f;
+  int64_t nx, ny, ntx, nty;
+  int off, periodic;
+  int kxl, kxh, kyl, kyh;
+  double gxl, gxh, gyl, gyh;
+  int mx, my, npts;
+  const double* ex;   // Ex[p][sx*(mx+1)+k] = sum_a (xg_p/2)^a M_x[a][sx*(mx+1)+k]
+  const double* ey;
+  const double* gw;   // Gauss weights
+  const double* gx;   // Gauss nodes on [-1,1]
+  int exact_kind;
+  const double* exact;  // [ci][cj][p][q]
+  double prm[4];
+  double x0, y0, hx, hy, coff;  // target node coordinates x0 + hx (i + coff)
+  double* part;
+};
+
+__device__ inline double exact_builtin(int kind, const double* prm, double x, double y) {
+  if (kind == 1) return sin(prm[0] * (x + y + sqrt(2.0) * prm[1]));  // driver.py:393-394
+  return sin(prm[0] * x) * sin(prm[1] * y) * cos(prm[2] * prm[3]);
+}
+
+// diagnostics.py:118-135 l2_error_field_2d: one thread per target cell.
+__global__ void l2err2d_kernel(L2Err2DArgs a) {
+  __shared__ double sh[kRedThreads];
+  const int64_t ncell = a.ntx * a.nty;
+  const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double local = 0.0;
+  if (cell < ncell) {
+    const int64_t ti = cell / a.nty, tj = cell - ti * a.nty;
+    const int mx = a.mx, my = a.my, wx = mx + 1, wy = my + 1, P = wx * wy;
+    const RowRef r0 = resolve_row(a.f, ti + a.off, a.nx, a.ny * P, a.periodic, a.kxl, a.kxh, a.gxl, a.gxh);
+    const RowRef r1 = resolve_row(a.f, ti + a.off + 1, a.nx, a.ny * P, a.periodic, a.kxl, a.kxh, a.gxl, a.gxh);
+    const ColRef c0 = resolve_col(tj + a.off, a.ny, a.periodic, a.kyl, a.kyh, a.gyl, a.gyh);
+    const ColRef c1 = resolve_col(tj + a.off + 1, a.ny, a.periodic, a.kyl, a.kyh, a.gyl, a.gyh);
+    const RowRef* rr[2] = {&r0, &r1};
+    const ColRef* cc[2] = {&c0, &c1};
+    const double cx = a.x0 + a.hx * ((double)ti + a.coff);
+    const double cy = a.y0 + a.hy * ((double)tj + a.coff);
+    double T[2 * 13];
+    for (int q = 0; q < a.npts; ++q) {
+      // T[sx][k] = sum_{sy,l} Ey[q][sy,l] U[sx][sy][k][l]
+      for (int sx = 0; sx < 2; ++sx)
+        for (int k = 0; k < wx; ++k) {
+          double s = 0.0;
+          for (int sy = 0; sy < 2; ++sy)
+            for (int l = 0; l < wy; ++l) {
+              double val = rr[sx]->p[cc[sy]->c * P + k * wy + l];
+              if (rr[sx]->kind | cc[sy]->kind)
+                val = ghosted(val, k, l, rr[sx]->kind, rr[sx]->g, cc[sy]->kind, cc[sy]->g);
+              s = fma(__ldg(a.ey + q * 2 * wy + sy * wy + l), val, s);
+            }
+          T[sx * wx + k] = s;
+        }
+      const double yq = cy + 0.5 * a.hy * a.gx[q];
+      for (int p = 0; p < a.npts; ++p) {
+        double val = 0.0;
+        for (int e = 0; e < 2 * wx; ++e) val = fma(__ldg(a.ex + p * 2 * wx + e), T[e], val);
+        double ex;
+        if (a.exact_kind == 0) {
+          ex = a.exact[((ti * a.nty + tj) * a.npts + p) * a.npts + q];
+        } else {
+          const double xp = cx + 0.5 * a.hx * a.gx[p];
+          ex = exact_builtin(a.exact_kind, a.prm, xp, yq);
+        }
+        const double d = val - ex;
+        local = fma(a.gw[p] * a.gw[q], d * d, local);
+      }
+    }
+  }
+  const double bs = block_sum(local, sh);
+  if (threadIdx.x == 0) a.part[blockIdx.x] = bs;
+}
+
+struct L2Err1DArgs {
+  const double* f;
+  int64_t n, nt;
+  int off, periodic, kl, kh;
+  double gl, gh;
+  int mu, deriv, npts;
+  double h;
+  const double* hl;
+  const double* xi;
+  const double* w;
+  const double* ex;
+  double* part;
+};
+
+// diagnostics.py:66-85 l2_error per piece (+ CellPolynomial eval/derivative).
+__global__ void l2err1d_kernel(L2Err1DArgs a) {
+  __shared__ double sh[kRedThreads];
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double local = 0.0;
+  if (t < a.nt) {
+    const int mu = a.mu;
+    double L[13], R[13], c[26];
+    for (int side = 0; side < 2; ++side) {
+      int64_t s = t + a.off + side;
+      int kind = 0;
+      double g = 0.0;
+      if (s < 0 || s >= a.n) {
+        if (a.periodic) s = pmod(s, a.n);
+        else if (s < 0) { s = 0; kind = a.kl; g = a.gl; }
+        else { s = a.n - 1; kind = a.kh; g = a.gh; }
+      }
+      double* dst = side ? R : L;
+      for (int l = 0; l <= mu; ++l) {
+        double val = a.f[s * (mu + 1) + l];
+        if (kind) {
+          val *= refl_sign(kind, l);
+          if (l == 0 && kind == HW_DIRICHLET0) val += 2.0 * g;
+        }
+        dst[l] = val;
+      }
+    }
+    const int nc = 2 * mu + 2;
+    for (int q = 0; q < nc; ++q) {
+      double s = 0.0;
+      for (int k = 0; k <= mu; ++k) {
+        const double comb = ((q + k) & 1) ? L[k] - R[k] : L[k] + R[k];
+        s = fma(a.hl[q * (mu + 1) + k], comb, s);
+      }
+      c[q] = s;
+    }
+    int deg = nc - 1;
+    if (a.deriv == 1) {  // poly.py:56-74 derivative(1): a[1:] * j / h
+      for (int j = 0; j < nc - 1; ++j) c[j] = c[j + 1] * (double)(j + 1) / a.h;
+      deg = nc - 2;
+    }
+    for (int p = 0; p < a.npts; ++p) {
+      const double x = a.xi[t * a.npts + p];
+      double v = c[deg];
+      for (int j = deg - 1; j >= 0; --j) v = v * x + c[j];  // poly.py:47-54 Horner
+      const double d = v - a.ex[t * a.npts + p];
+      local = fma(a.w[t * a.npts + p], d * d, local);
+    }
+  }
+  const double bs = block_sum(local, sh);
+  if (threadIdx.x == 0) a.part[blockIdx.x] = bs;
+}
+
+__global__ void nonfinite_kernel(const double* x, int64_t n, unsigned long long* cnt) {
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(x[i])) ++c;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, c);
+}
+
+// driver.py:241-256 planewave_data / standing wave, one thread per node.
+struct Init2DArgs {
+  double* out;
+  int64_t nx, ny;
+  int kx, ky;
+  double x0, y0, off, t, hx, hy;
+  int kind;  // 1 plane wave, 2 standing wave
+  double w;  // plane wave: 2 pi kappa
+  double ax, ay, px, py, om;
+  int tder;
+};
+
+__global__ void init2d_kernel(Init2DArgs a) {
+  const int64_t node = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= a.nx * a.ny) return;
+  const int64_t i = node / a.ny, j = node - i * a.ny;
+  const double x = a.x0 + a.hx * ((double)i + a.off);
+  const double y = a.y0 + a.hy * ((double)j + a.off);
+  const int wx = a.kx + 1, wy = a.ky + 1;
+  double* o = a.out + node * wx * wy;
+  const double hpi = 0.5 * 3.141592653589793;
+  if (a.kind == 1) {
+    const double th = a.w * (x + y + sqrt(2.0) * a.t);
+    for (int k = 0; k < wx; ++k) {
+      double fk = 1.0;
+      for (int q = 2; q <= k; ++q) fk *= q;
+      for (int l = 0; l < wy; ++l) {
+        double fl = 1.0;
+        for (int q = 2; q <= l; ++q) fl *= q;
+        double amp = pow(a.w, (double)(k + l)) * pow(sqrt(2.0) * a.w, (double)a.tder);
+        amp *= pow(a.hx, (double)k) / fk * pow(a.hy, (double)l) / fl;
+        o[k * wy + l] = amp * sin(th + hpi * (double)(k + l + a.tder));
+      }
+    }
+  } else {
+    const double sxv = 0, syv = 0;
+    (void)sxv;
+    (void)syv;
+    for (int k = 0; k < wx; ++k) {
+      double fk = 1.0;
+      for (int q = 2; q <= k; ++q) fk *= q;
+      const double dx = pow(a.ax, (double)k) * sin(a.ax * x + a.px + hpi * k) * pow(a.hx, (double)k) / fk;
+      for (int l = 0; l < wy; ++l) {
+        double fl = 1.0;
+        for (int q = 2; q <= l; ++q) fl *= q;
+        const double dy = pow(a.ay, (double)l) * sin(a.ay * y + a.py + hpi * l) * pow(a.hy, (double)l) / fl;
+        const double dt = pow(a.om, (double)a.tder) * cos(a.om * a.t + hpi * a.tder);
+        o[k * wy + l] = dx * dy * dt;
+      }
+    }
+  }
+}
+
+}  // namespace hw

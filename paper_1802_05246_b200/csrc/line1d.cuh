@@ -1,0 +1,168 @@
+// 1D steps: one thread per target node.  The 1D path is small (config C1 is
+// n = 200) so these kernels follow the reference's stage recursion literally
+// (dissipative.py:77-106, conservative.py:77-84,115-127,166-184) with the
+// interpolation done by the parity-split Hermite left block.
+#pragma once
+
+#include "common.cuh"
+
+namespace hw {
+
+constexpr int kMax1D = 12;
+constexpr int kMaxStages1D = 2 * kMax1D + 4;
+
+struct Line1DArgs {
+  const double* u;  // source field (order mu_u)
+  const double* v;  // second source (order mu_v) or null
+  const double* prev;
+  const double* forcing;  // F[s-1][l][t]
+  double* ou;
+  double* ov;
+  int64_t n, nt;   // source nodes, targets
+  int off, periodic;
+  int kl, kh;
+  double gl, gh;   // Dirichlet data of u (v reflects around 0)
+  int m;
+  int stages;
+  double dt, h, speed, rho;
+  const double* hl_u;  // device HL_{mu_u}: (2mu+2) x (mu+1)
+  const double* hl_v;
+};
+
+// Flanking data of target t: left/right source nodes with ghosts.
+__device__ inline void load_pair(const double* f, int mu, int64_t t, const Line1DArgs& a, double gl,
+                                 double gh, double* L, double* R) {
+  const int64_t s0 = t + a.off;
+#pragma unroll 1
+  for (int side = 0; side < 2; ++side) {
+    int64_t s = s0 + side;
+    int kind = 0;
+    double g = 0.0;
+    if (s < 0 || s >= a.n) {
+      if (a.periodic) {
+        s = pmod(s, a.n);
+      } else if (s < 0) {
+        s = 0;
+        kind = a.kl;
+        g = gl;
+      } else {
+        s = a.n - 1;
+        kind = a.kh;
+        g = gh;
+      }
+    }
+    double* dst = side ? R : L;
+    for (int l = 0; l <= mu; ++l) {
+      double val = f[s * (mu + 1) + l];
+      if (kind) {  // boundary.py:65-76 ghost_data
+        val *= refl_sign(kind, l);
+        if (l == 0 && kind == HW_DIRICHLET0) val += 2.0 * g;
+      }
+      dst[l] = val;
+    }
+  }
+}
+
+// Interpolant coefficients c[0..2mu+1] from (L, R) via the left block:
+// c[a] = sum_k HL[a][k] (L[k] + (-1)^(a+k) R[k])   (interp.py:78-90)
+__device__ inline void interp1d(const double* hl, int mu, const double* L, const double* R, double* c) {
+  for (int a = 0; a < 2 * mu + 2; ++a) {
+    double s = 0.0;
+    for (int k = 0; k <= mu; ++k) {
+      const double comb = ((a + k) & 1) ? L[k] - R[k] : L[k] + R[k];
+      s = fma(hl[a * (mu + 1) + k], comb, s);
+    }
+    c[a] = s;
+  }
+}
+
+// dissipative.py:160-181 half_step_1d
+__global__ void diss1d_kernel(Line1DArgs a) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= a.nt) return;
+  const int m = a.m;
+  double L[kMax1D + 1], R[kMax1D + 1];
+  double cu[2 * kMax1D + 2], cv[2 * kMax1D + 2];
+  load_pair(a.u, m, t, a, a.gl, a.gh, L, R);
+  interp1d(a.hl_u, m, L, R, cu);
+  load_pair(a.v, m - 1, t, a, 0.0, 0.0, L, R);
+  interp1d(a.hl_v, m - 1, L, R, cv);
+  const int lu = 2 * m + 2, lv = 2 * m;
+  const int nsrc = lv < lu - 2 ? lv : lu - 2;
+  const double r = a.speed * a.speed * a.dt / (a.h * a.h);
+  // forward accumulation of the theta-series (theta = 1/2: powers are exact)
+  double ou[kMax1D + 1], ov[kMax1D + 1];
+  for (int l = 0; l <= m; ++l) ou[l] = cu[l];
+  for (int l = 0; l < m; ++l) ov[l] = cv[l];
+  double pw = 1.0;
+  double nc[2 * kMax1D + 2], nd[2 * kMax1D + 2];
+  for (int s = 1; s <= a.stages; ++s) {
+    pw *= 0.5;
+    const double fdt = a.dt / s, fr = r / s;
+    for (int l = 0; l < lu; ++l) nc[l] = l < lv ? fdt * cv[l] : 0.0;
+    for (int l = 0; l < lv; ++l) nd[l] = l < nsrc ? (fr * (double)((l + 2) * (l + 1))) * cu[l + 2] : 0.0;
+    if (a.forcing) {
+      for (int l = 0; l < lv; ++l) nd[l] += a.forcing[((int64_t)(s - 1) * lv + l) * a.nt + t];
+    }
+    for (int l = 0; l < lu; ++l) cu[l] = nc[l];
+    for (int l = 0; l < lv; ++l) cv[l] = nd[l];
+    for (int l = 0; l <= m; ++l) ou[l] = fma(pw, cu[l], ou[l]);
+    for (int l = 0; l < m; ++l) ov[l] = fma(pw, cv[l], ov[l]);
+  }
+  for (int l = 0; l <= m; ++l) a.ou[t * (m + 1) + l] = ou[l];
+  for (int l = 0; l < m; ++l) a.ov[t * m + l] = ov[l];
+}
+
+// conservative.py:115-127 conservative_update_1d: new = 2 W c - prev,
+// W[k][j] = C(j,k) rho^(j-k), j = k, k+2, ... <= 2m+1.
+__global__ void cons1d_kernel(Line1DArgs a) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= a.nt) return;
+  const int m = a.m;
+  double L[kMax1D + 1], R[kMax1D + 1], c[2 * kMax1D + 2];
+  load_pair(a.u, m, t, a, a.gl, a.gh, L, R);
+  interp1d(a.hl_u, m, L, R, c);
+  for (int k = 0; k <= m; ++k) {
+    double s = 0.0;
+    double binom = 1.0, rp = 1.0;  // C(j,k), rho^(j-k) for j = k
+    for (int j = k; j < 2 * m + 2; j += 2) {
+      s = fma(binom * rp, c[j], s);
+      // advance j -> j+2: C(j+2,k) = C(j,k) (j+2)(j+1) / ((j+2-k)(j+1-k))
+      binom = binom * (double)((j + 2) * (j + 1)) / (double)((j + 2 - k) * (j + 1 - k));
+      rp *= a.rho * a.rho;
+    }
+    a.ou[t * (m + 1) + k] = 2.0 * s - a.prev[t * (m + 1) + k];
+  }
+}
+
+// conservative.py:166-184 bootstrap_first_half (1D): expand_taylor on I_m g0,
+// I_m g1 with 2m+3 stages, u at theta = 1/2 truncated to order m.
+__global__ void boot1d_kernel(Line1DArgs a) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= a.nt) return;
+  const int m = a.m;
+  double L[kMax1D + 1], R[kMax1D + 1];
+  double cu[2 * kMax1D + 2], cv[2 * kMax1D + 2], nc[2 * kMax1D + 2], nd[2 * kMax1D + 2];
+  load_pair(a.u, m, t, a, a.gl, a.gh, L, R);
+  interp1d(a.hl_u, m, L, R, cu);
+  load_pair(a.v, m, t, a, 0.0, 0.0, L, R);
+  interp1d(a.hl_u, m, L, R, cv);
+  const int lu = 2 * m + 2, lv = 2 * m + 2;
+  const int nsrc = lv < lu - 2 ? lv : lu - 2;
+  const double r = a.speed * a.speed * a.dt / (a.h * a.h);
+  double ou[kMax1D + 1];
+  for (int l = 0; l <= m; ++l) ou[l] = cu[l];
+  double pw = 1.0;
+  for (int s = 1; s <= a.stages; ++s) {
+    pw *= 0.5;
+    const double fdt = a.dt / s, fr = r / s;
+    for (int l = 0; l < lu; ++l) nc[l] = fdt * cv[l];
+    for (int l = 0; l < lv; ++l) nd[l] = l < nsrc ? (fr * (double)((l + 2) * (l + 1))) * cu[l + 2] : 0.0;
+    for (int l = 0; l < lu; ++l) cu[l] = nc[l];
+    for (int l = 0; l < lv; ++l) cv[l] = nd[l];
+    for (int l = 0; l <= m; ++l) ou[l] = fma(pw, cu[l], ou[l]);
+  }
+  for (int l = 0; l <= m; ++l) a.ou[t * (m + 1) + l] = ou[l];
+}
+
+}  // namespace hw

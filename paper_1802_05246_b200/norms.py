@@ -1,0 +1,217 @@
+"""Error norms and rate fitting (drop-in for the L2 parts of hermwave.diagnostics).
+
+The per-cell interpolation, Gauss evaluation and the reduction run on the
+device (csrc/diag.cuh).  What stays on the host is geometry only: Gauss rules,
+piece clipping and — for a user-supplied Python ``exact`` callable — its
+evaluation at the quadrature points, exactly as the reference evaluates it
+(diagnostics.py:66-85,118-135).  Built-in closed forms (``PlaneWave2D``,
+``StandingWave2D``) are evaluated inside the kernel.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib as L
+from .config import BoundarySpec, BoundarySpec2D, check_periodicity
+from .device import Staging, ptr
+from .fields import DUAL, PRIMAL, Field1D, Field2D, FieldPair, flip
+from .stepping import _PARITY, geom2d, rows2d
+
+
+def gauss_rule(npts: int):
+    """Gauss-Legendre nodes/weights on [-1, 1] (diagnostics.py:33-35)."""
+    return np.polynomial.legendre.leggauss(npts)
+
+
+def default_npts(m: int) -> int:
+    """diagnostics.py:38-40."""
+    return 2 * m + 2
+
+
+@dataclass(frozen=True)
+class PlaneWave2D:
+    """u = sin(w (x + y + sqrt(2) t)), w = 2 pi kappa (driver.py:381,393-394)."""
+
+    kappa: float
+    t: float
+
+    def __call__(self, x, y):
+        w = 2.0 * np.pi * self.kappa
+        return np.sin(w * (x + y + math.sqrt(2.0) * self.t))
+
+    @property
+    def device_form(self):
+        return 1, (2.0 * np.pi * self.kappa, self.t, 0.0, 0.0)
+
+
+@dataclass(frozen=True)
+class StandingWave2D:
+    """u = sin(ax x) sin(ay y) cos(om t) (SURVEY §8d throughput data)."""
+
+    ax: float
+    ay: float
+    om: float
+    t: float
+
+    def __call__(self, x, y):
+        return np.sin(self.ax * x) * np.sin(self.ay * y) * math.cos(self.om * self.t)
+
+    @property
+    def device_form(self):
+        return 2, (self.ax, self.ay, self.om, self.t)
+
+
+def l2_error_field_2d(field: Field2D, exact, bc: BoundarySpec2D, npts: int | None = None) -> float:
+    """L2 error of the global tensor interpolant (diagnostics.py:118-135).
+
+    Like the reference, cells are the targets of the field's own corner
+    gather (no clipping in 2D)."""
+    mx, my = field.orders
+    npts = npts or default_npts(max(mx, my))
+    grid = field.grid
+    g = geom2d(grid, field.parity, bc)
+    xg, wg = gauss_rule(npts)
+    st = Staging(field.values)
+    f = st.to_dev(field.values)
+    params = (C.c_double * 4)(0.0, 0.0, 0.0, 0.0)
+    ex_dev = None
+    form = getattr(exact, "device_form", None)
+    if form is not None:
+        kind, prm = form
+        for i, p in enumerate(prm):
+            params[i] = float(p)
+    else:
+        kind = 0
+        cx = grid.axis(0).nodes(flip(field.parity))
+        cy = grid.axis(1).nodes(flip(field.parity))
+        x = cx[:, None] + 0.5 * grid.hx * xg[None, :]
+        y = cy[:, None] + 0.5 * grid.hy * xg[None, :]
+        ex = np.broadcast_to(exact(x[:, None, :, None], y[None, :, None, :]),
+                             (len(cx), len(cy), npts, npts))
+        ex_dev = st.to_dev(np.ascontiguousarray(ex))
+    gx = np.ascontiguousarray(xg, dtype=np.float64)
+    gw = np.ascontiguousarray(wg, dtype=np.float64)
+    out = C.c_double(0.0)
+    L.check(L.lib().hw_l2err2d(C.byref(rows2d(f)), int(mx), int(my), C.byref(g), float(grid.x_left),
+                               float(grid.y_left), grid.hx, grid.hy, int(npts), gx.ctypes.data_as(C.c_void_p),
+                               gw.ctypes.data_as(C.c_void_p), int(kind),
+                               ptr(ex_dev) if ex_dev is not None else None, params, C.byref(out), st.stream),
+            "l2_error_field_2d")
+    return math.sqrt(out.value)
+
+
+def _pieces_1d(field: Field1D):
+    """Target centres and breakpoints of the global interpolant (diagnostics.py:47-59)."""
+    grid = field.grid
+    centers = grid.nodes(flip(field.parity))
+    h = grid.h
+    bp = np.concatenate([centers - 0.5 * h, centers[-1:] + 0.5 * h])
+    return centers, bp, h
+
+
+def _domain_clip(field):
+    if field.grid.periodic:
+        return None
+    return field.grid.x_left, field.grid.x_right
+
+
+def _quadrature_1d(field: Field1D, exact, npts: int, clip):
+    """Per-piece scaled abscissae, weights and exact values (diagnostics.py:74-85)."""
+    centers, bp, h = _pieces_1d(field)
+    xg, wg = gauss_rule(npts)
+    n = len(centers)
+    xi = np.zeros((n, npts))
+    w = np.zeros((n, npts))
+    ex = np.zeros((n, npts))
+    for i in range(n):
+        a, b = bp[i], bp[i + 1]
+        if clip is not None:
+            a, b = max(a, clip[0]), min(b, clip[1])
+            if b <= a:
+                continue
+        x = 0.5 * (a + b) + 0.5 * (b - a) * xg
+        xi[i] = (x - centers[i]) / h
+        w[i] = 0.5 * (b - a) * wg
+        ex[i] = exact(x)
+    return xi, w, ex
+
+
+def _l2_1d(field: Field1D, bc: BoundarySpec, quad, deriv: int, st: Staging) -> float:
+    grid = field.grid
+    check_periodicity(bc, grid.periodic)
+    xi, w, ex = quad
+    npts = xi.shape[1]
+    f = st.to_dev(field.values)
+    dxi, dw, dex = st.to_dev(xi), st.to_dev(w), st.to_dev(ex)
+    abc = L.axis_bc(bc)
+    out = C.c_double(0.0)
+    L.check(L.lib().hw_l2err1d(ptr(f), int(field.order), grid.n_nodes(field.parity), _PARITY[field.parity],
+                               C.byref(abc), grid.h, int(deriv), int(npts), ptr(dxi), ptr(dw), ptr(dex),
+                               C.byref(out), st.stream), "l2_error")
+    return math.sqrt(max(out.value, 0.0))
+
+
+def l2_error_field(field: Field1D, exact, bc: BoundarySpec, npts: int | None = None) -> float:
+    """diagnostics.py:96-100."""
+    npts = npts or default_npts(field.order)
+    st = Staging(field.values)
+    quad = _quadrature_1d(field, exact, npts, _domain_clip(field))
+    return _l2_1d(field, bc, quad, 0, st)
+
+
+def l2_errors_pair(pair: FieldPair, exact_u, exact_dux, exact_v, bc: BoundarySpec,
+                   npts: int | None = None):
+    """(u, u_x, v) errors of a dissipative state (diagnostics.py:103-115)."""
+    m = pair.u.order
+    npts = npts or default_npts(m)
+    clip = _domain_clip(pair.u)
+    st = Staging(pair.u.values, pair.v.values)
+    qu = _quadrature_1d(pair.u, exact_u, npts, clip)
+    qd = _quadrature_1d(pair.u, exact_dux, npts, clip)
+    qv = _quadrature_1d(pair.v, exact_v, npts, clip)
+    return (_l2_1d(pair.u, bc, qu, 0, st), _l2_1d(pair.u, bc, qd, 1, st), _l2_1d(pair.v, bc, qv, 0, st))
+
+
+@dataclass(frozen=True)
+class ErrorReport:
+    """Refinement-study results, coarsest first (diagnostics.py:241-270)."""
+
+    ns: np.ndarray
+    hs: np.ndarray
+    dts: np.ndarray
+    err_u: np.ndarray
+    err_dux: np.ndarray | None = None
+    err_v: np.ndarray | None = None
+
+    def __post_init__(self):
+        if np.any(np.diff(self.hs) >= 0):
+            raise ValueError("refinement levels must have strictly decreasing h")
+        for e in (self.err_u, self.err_dux, self.err_v):
+            if e is not None and not np.all(e > 0):
+                raise ValueError("error norms must be positive")
+
+    def pair_rates(self) -> np.ndarray:
+        e, h = self.err_u, self.hs
+        return np.log(e[:-1] / e[1:]) / np.log(h[:-1] / h[1:])
+
+    def rate(self) -> float:
+        return fit_rate(self.hs, self.err_u)
+
+
+def fit_rate(hs, errors) -> float:
+    """Least-squares log-log slope over the ceil(L/2) finest levels (diagnostics.py:263-278)."""
+    hs = np.asarray(hs, dtype=float)
+    errors = np.asarray(errors, dtype=float)
+    if len(hs) < 3:
+        raise ValueError(f"rate fit needs at least 3 levels, got {len(hs)}")
+    k = (len(hs) + 1) // 2
+    return float(np.polyfit(np.log(hs[-k:]), np.log(errors[-k:]), 1)[0])
+
+
+__all__ = ["gauss_rule", "default_npts", "PlaneWave2D", "StandingWave2D", "l2_error_field_2d",
+           "l2_error_field", "l2_errors_pair", "ErrorReport", "fit_rate", "PRIMAL", "DUAL"]
