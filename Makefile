@@ -6,7 +6,7 @@ SRC := paper_1802_05246_b200/csrc
 LIB := paper_1802_05246_b200/libhermb200.so
 OBJ := build/capi.o build/tables.o
 
-all: $(LIB)
+all: $(LIB) tools/fp64_peak
 
 build/capi.o: $(SRC)/capi.cu $(wildcard $(SRC)/*.cuh) $(SRC)/tables.h include/hermb200.h
 	@mkdir -p build
@@ -22,4 +22,9 @@ $(LIB): $(OBJ)
 clean:
 	rm -rf build $(LIB)
 
-.PHONY: all clean
+.PHONY: all clean tools
+
+tools/fp64_peak: tools/fp64_peak.cu
+	$(NVCC) $(ARCH) -O3 -o $@ $<
+
+tools: tools/fp64_peak

@@ -111,7 +111,7 @@ int hw_boot2d(const hw_rows2d* g0_src, const hw_rows2d* g1_src, double* out,
 
 /*
  * dissipative.py:160-181 half_step_1d.  forcing (may be NULL) is a device
- * array F[s-1][l][t] (s = 1..stages, l < m, t < n_targets) of the already
+ * array F[s-1][l][t] (s = 1..stages, l < 2m, t < n_targets) of the already
  * scaled terms h^l dt^s/(l! s!) f(l, s-1, x_t, time) (dissipative.py:102-105).
  */
 int hw_diss1d_half_step(const double* u_src, const double* v_src,

@@ -116,14 +116,18 @@ static void launch_diss2d(const Step2DArgs& a, double dt, double rx, double ry, 
   for (int k = 0; k <= M; ++k)
     for (int l = 0; l <= M; ++l) T.inv[k][l] = 1.0 / (px[k] * py[l]);
 
-  using S_ = Diss2DSmem<M>;
-  const int smem = S_::bytes + kTileJ * (S_::PU + S_::PV) * 8;
+  const int smem = diss2d_smem_bytes<M>();
   cuda_check(cudaFuncSetAttribute(diss2d_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
              "cudaFuncSetAttribute(diss2d)");
-  const int64_t nct = (a.nty + kTileJ - 1) / kTileJ;
-  const int64_t gy = a.ntrows < 65535 ? a.ntrows : 65535;
-  dim3 grid((unsigned)nct, (unsigned)gy);
-  diss2d_kernel<M><<<grid, 128, smem, st>>>(P);
+  int dev = 0, nsm = 0, per_sm = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  cuda_check(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "sm count");
+  constexpr int TR = tile_rows<M>();
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, diss2d_kernel<M>, 32 * TR, smem), "occupancy");
+  const int64_t ntiles = ((a.nty + kTileJ - 1) / kTileJ) * ((a.ntrows + TR - 1) / TR);
+  int64_t nblk = (int64_t)nsm * (per_sm > 0 ? per_sm : 1);
+  if (nblk > ntiles) nblk = ntiles;
+  diss2d_kernel<M><<<(unsigned)nblk, 32 * TR, smem, st>>>(P);
   cuda_check(cudaGetLastError(), "diss2d launch");
 }
 

@@ -122,10 +122,15 @@ __device__ __forceinline__ void taps(const double (&d)[M], const int b, const do
 }
 
 template <int M, int PA, int PB>
-__device__ __forceinline__ void diss2d_class(const Diss2DTables<M>& T, const double* __restrict__ su,
-                                             const double* __restrict__ sv, double* __restrict__ ou,
-                                             double* __restrict__ ov, int lane) {
+__device__ __forceinline__ void diss2d_class(const Diss2DTables<M>& T, const double* __restrict__ u00,
+                                             const double* __restrict__ u10, const double* __restrict__ v00,
+                                             const double* __restrict__ v10, double* __restrict__ ou,
+                                             double* __restrict__ ov) {
   using S = Diss2DSmem<M>;
+  const double* u01 = u00 + S::PUP;
+  const double* u11 = u10 + S::PUP;
+  const double* v01 = v00 + S::PVP;
+  const double* v11 = v10 + S::PVP;
   constexpr int NKU = (M - PA) / 2 + 1, NLU = (M - PB) / 2 + 1;
   constexpr int NKV = (M - 1 - PA) / 2 + 1, NLV = (M - 1 - PB) / 2 + 1;
   constexpr int NA = M;  // rows a = PA + 2 ia of the 2M-row arrays
@@ -142,10 +147,6 @@ __device__ __forceinline__ void diss2d_class(const Diss2DTables<M>& T, const dou
 
   // ---- sweep V: d0 = I_{m-1,m-1} v (phi-scaled), taps A (u) and Gamma (v)
   {
-    const double* v00 = sv + (0 * S::NQ + lane) * S::PVP;
-    const double* v01 = sv + (0 * S::NQ + lane + 1) * S::PVP;
-    const double* v10 = sv + (1 * S::NQ + lane) * S::PVP;
-    const double* v11 = sv + (1 * S::NQ + lane + 1) * S::PVP;
     double G[M][M];
 #pragma unroll
     for (int k = 0; k < M; ++k)
@@ -184,10 +185,6 @@ __device__ __forceinline__ void diss2d_class(const Diss2DTables<M>& T, const dou
 
   // ---- sweep U: cmm (low block), c_x = I_{m,m-1} u, c_y = I_{m-1,m} u
   {
-    const double* u00 = su + (0 * S::NQ + lane) * S::PUP;
-    const double* u01 = su + (0 * S::NQ + lane + 1) * S::PUP;
-    const double* u10 = su + (1 * S::NQ + lane) * S::PUP;
-    const double* u11 = su + (1 * S::NQ + lane + 1) * S::PUP;
     double G[M + 1][M + 1];
 #pragma unroll
     for (int k = 0; k <= M; ++k)
@@ -260,68 +257,173 @@ __device__ __forceinline__ void diss2d_class(const Diss2DTables<M>& T, const dou
     }
   }
 
-  // ---- unscale and store this class's coefficients
+  // ---- unscale and store this class's coefficients (straight to global)
+  if (ou == nullptr) return;
 #pragma unroll
   for (int x = 0; x < NKU; ++x)
 #pragma unroll
     for (int y = 0; y < NLU; ++y) {
       const int k = PA + 2 * x, l = PB + 2 * y;
-      ou[lane * (M + 1) * (M + 1) + k * (M + 1) + l] = T.inv[k][l] * au[x][y];
+      ou[k * (M + 1) + l] = T.inv[k][l] * au[x][y];
     }
 #pragma unroll
   for (int x = 0; x < NKV; ++x)
 #pragma unroll
     for (int y = 0; y < NLV; ++y) {
       const int k = PA + 2 * x, l = PB + 2 * y;
-      if (k < M && l < M) ov[lane * M * M + k * M + l] = T.inv[k][l] * av[x][y];
+      if (k < M && l < M) ov[k * M + l] = T.inv[k][l] * av[x][y];
     }
 }
 
+// Async 8-byte global->shared copy (LDGSTS); completion tracked per thread
+// with commit/wait groups.
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Target rows per tile (= warps per CTA, one row per warp).  The staged
+// source block is double buffered, so large orders use fewer rows to fit.
 template <int M>
-__global__ void __launch_bounds__(128) diss2d_kernel(const __grid_constant__ Diss2DParams<M> P) {
-  using S = Diss2DSmem<M>;
-  extern __shared__ __align__(16) double smem[];
-  double* su = smem;
-  double* sv = smem + 2 * S::NQ * S::PUP;
-  const Step2DArgs& a = P.a;
-  const int64_t j0 = (int64_t)blockIdx.x * kTileJ;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int PU = S::PU, PV = S::PV;
+constexpr int tile_rows() {
+  return M <= 4 ? 4 : (M <= 6 ? 2 : 1);
+}
 
-  for (int64_t tr = blockIdx.y; tr < a.ntrows; tr += gridDim.y) {
-    const int64_t t = a.trow0 + tr;
-    const int64_t s0 = t + a.off;
-    const RowRef ru0 = resolve_row(a.u, s0, a.nx, a.ny * PU, a.periodic, a.kxl, a.kxh, a.gxl, a.gxh);
-    const RowRef ru1 = resolve_row(a.u, s0 + 1, a.nx, a.ny * PU, a.periodic, a.kxl, a.kxh, a.gxl, a.gxh);
-    const RowRef rv0 = resolve_row(a.v, s0, a.nx, a.ny * PV, a.periodic, a.kxl, a.kxh, 0.0, 0.0);
-    const RowRef rv1 = resolve_row(a.v, s0 + 1, a.nx, a.ny * PV, a.periodic, a.kxl, a.kxh, 0.0, 0.0);
-    __syncthreads();  // previous iteration's output copy-out done
-    stage_rows<PU, S::PUP, M + 1>(su, ru0, ru1, j0 + a.off, a, true);
-    stage_rows<PV, S::PVP, M>(sv, rv0, rv1, j0 + a.off, a, false);
-    __syncthreads();
-
-    // outputs staged in registers, then written through smem for coalescing
-    double* ou = smem;                       // reuse after the barrier below
-    double* ov = smem + kTileJ * PU;
-    // compute into registers first (sources are read inside); we need the raw
-    // rows intact until every warp is done, so results go to a second region.
-    double* ou2 = smem + 2 * S::NQ * S::PUP + 2 * S::NQ * S::PVP;
-    double* ov2 = ou2 + kTileJ * PU;
-    switch (warp) {
-      case 0: diss2d_class<M, 0, 0>(P.t, su, sv, ou2, ov2, lane); break;
-      case 1: diss2d_class<M, 0, 1>(P.t, su, sv, ou2, ov2, lane); break;
-      case 2: diss2d_class<M, 1, 0>(P.t, su, sv, ou2, ov2, lane); break;
-      default: diss2d_class<M, 1, 1>(P.t, su, sv, ou2, ov2, lane); break;
+// Issue the async copies of one tile's source block (kTileRows+1 rows x 33
+// nodes) of one field into shared memory.  Ghost/wrapped nodes are copied
+// from their mirror source; reflection signs are applied after arrival.
+template <int P, int PP, int TR>
+__device__ inline void issue_tile(double* __restrict__ dst, const Rows& R, int64_t s_first, int64_t c_first,
+                                  const Step2DArgs& a) {
+  constexpr int NQ = kTileJ + 1;
+  for (int r = 0; r <= TR; ++r) {
+    const RowRef rr = resolve_row(R, s_first + r, a.nx, a.ny * P, a.periodic, a.kxl, a.kxh, 0.0, 0.0);
+    for (int idx = threadIdx.x; idx < NQ * P; idx += blockDim.x) {
+      const int q = idx / P;
+      const int e = idx - q * P;
+      const ColRef cc = resolve_col(c_first + q, a.ny, a.periodic, a.kyl, a.kyh, 0.0, 0.0);
+      cp_async8(dst + (r * NQ + q) * PP + e, rr.p + cc.c * P + e);
     }
-    (void)ou;
-    (void)ov;
-    __syncthreads();
-    const int64_t ncols = (a.nty - j0) < kTileJ ? (a.nty - j0) : kTileJ;
-    double* gu = a.ud + (tr * a.nty + j0) * PU;
-    double* gv = a.vd + (tr * a.nty + j0) * PV;
-    for (int idx = threadIdx.x; idx < ncols * PU; idx += blockDim.x) gu[idx] = ou2[idx];
-    for (int idx = threadIdx.x; idx < ncols * PV; idx += blockDim.x) gv[idx] = ov2[idx];
   }
+}
+
+// Apply wall reflections to the ghost nodes of a staged tile (walls only).
+template <int P, int PP, int NL, int TR>
+__device__ inline void fix_ghosts(double* __restrict__ dst, int64_t s_first, int64_t c_first, const Step2DArgs& a,
+                                  bool is_u) {
+  constexpr int NQ = kTileJ + 1;
+  for (int idx = threadIdx.x; idx < (TR + 1) * NQ * P; idx += blockDim.x) {
+    const int r = idx / (NQ * P);
+    const int rem = idx - r * (NQ * P);
+    const int q = rem / P;
+    const int e = rem - q * P;
+    const int64_t s = s_first + r, c = c_first + q;
+    int xk = 0, yk = 0;
+    double gx = 0.0, gy = 0.0;
+    if (s < 0) { xk = a.kxl; gx = a.gxl; }
+    else if (s >= a.nx) { xk = a.kxh; gx = a.gxh; }
+    if (c < 0) { yk = a.kyl; gy = a.gyl; }
+    else if (c >= a.ny) { yk = a.kyh; gy = a.gyh; }
+    if (xk | yk) {
+      double* p = dst + (r * NQ + q) * PP + e;
+      *p = ghosted(*p, e / NL, e % NL, xk, is_u ? gx : 0.0, yk, is_u ? gy : 0.0);
+    }
+  }
+}
+
+// Persistent kernel: each CTA walks tiles of kTileRows x 32 target cells,
+// prefetching the next tile's source rows with cp.async while its four warps
+// compute the current one.  All warps run the same parity class at the same
+// time (warp w = tile row w), which keeps the instruction working set to one
+// class's code.
+template <int M>
+__global__ void __launch_bounds__(32 * tile_rows<M>(), M <= 4 ? 2 : 1)
+    diss2d_kernel(const __grid_constant__ Diss2DParams<M> P) {
+  using S = Diss2DSmem<M>;
+  constexpr int kTileRows = tile_rows<M>();
+  constexpr int PU = S::PU, PV = S::PV, NQ = S::NQ;
+  constexpr int BU = (kTileRows + 1) * NQ * S::PUP;  // doubles per u buffer
+  constexpr int BV = (kTileRows + 1) * NQ * S::PVP;
+  extern __shared__ __align__(16) double smem[];
+  const Step2DArgs& a = P.a;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tcols = (a.nty + kTileJ - 1) / kTileJ;
+  const int64_t trows = (a.ntrows + kTileRows - 1) / kTileRows;
+  const int64_t ntiles = tcols * trows;
+  const bool walls = !a.periodic;
+
+  auto tile_origin = [&](int64_t tile, int64_t& tr0, int64_t& j0) {
+    const int64_t ti = tile / tcols;
+    tr0 = ti * kTileRows;
+    j0 = (tile - ti * tcols) * kTileJ;
+  };
+  auto issue = [&](int64_t tile, int b) {
+    int64_t tr0, j0;
+    tile_origin(tile, tr0, j0);
+    const int64_t s_first = a.trow0 + tr0 + a.off, c_first = j0 + a.off;
+    issue_tile<PU, S::PUP, kTileRows>(smem + b * (BU + BV), a.u, s_first, c_first, a);
+    issue_tile<PV, S::PVP, kTileRows>(smem + b * (BU + BV) + BU, a.v, s_first, c_first, a);
+    cp_async_commit();
+  };
+
+  int b = 0;
+  int64_t tile = blockIdx.x;
+  if (tile < ntiles) issue(tile, 0);
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int64_t next = tile + gridDim.x;
+    if (next < ntiles) {
+      issue(next, b ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    int64_t tr0, j0;
+    tile_origin(tile, tr0, j0);
+    double* su = smem + b * (BU + BV);
+    double* sv = su + BU;
+    if (walls) {
+      const int64_t s_first = a.trow0 + tr0 + a.off, c_first = j0 + a.off;
+      const bool edge = s_first < 0 || s_first + kTileRows >= a.nx || c_first < 0 || c_first + kTileJ >= a.ny;
+      if (edge) {
+        fix_ghosts<PU, S::PUP, M + 1, kTileRows>(su, s_first, c_first, a, true);
+        fix_ghosts<PV, S::PVP, M, kTileRows>(sv, s_first, c_first, a, false);
+        __syncthreads();
+      }
+    }
+    const int64_t tr = tr0 + warp;
+    const int64_t j = j0 + lane;
+    const bool valid = tr < a.ntrows && j < a.nty;
+    double* ou = valid ? a.ud + (tr * a.nty + j) * PU : nullptr;
+    double* ov = valid ? a.vd + (tr * a.nty + j) * PV : nullptr;
+    if (tr < a.ntrows) {
+      const double* u0 = su + (warp * NQ + lane) * S::PUP;
+      const double* u1 = u0 + NQ * S::PUP;
+      const double* v0 = sv + (warp * NQ + lane) * S::PVP;
+      const double* v1 = v0 + NQ * S::PVP;
+      // one class at a time: keeps live ranges (and the i-cache footprint) to one class
+#pragma unroll 1
+      for (int cls = 0; cls < 4; ++cls) {
+        switch (cls) {
+          case 0: diss2d_class<M, 0, 0>(P.t, u0, u1, v0, v1, ou, ov); break;
+          case 1: diss2d_class<M, 0, 1>(P.t, u0, u1, v0, v1, ou, ov); break;
+          case 2: diss2d_class<M, 1, 0>(P.t, u0, u1, v0, v1, ou, ov); break;
+          default: diss2d_class<M, 1, 1>(P.t, u0, u1, v0, v1, ou, ov); break;
+        }
+      }
+    }
+    __syncthreads();  // buffer b is refilled by the issue() of the next iteration
+    b ^= 1;
+  }
+}
+
+template <int M>
+constexpr int diss2d_smem_bytes() {
+  using S = Diss2DSmem<M>;
+  return 2 * (tile_rows<M>() + 1) * S::NQ * (S::PUP + S::PVP) * 8;
 }
 
 }  // namespace hw

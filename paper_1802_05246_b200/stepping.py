@@ -215,9 +215,11 @@ def bootstrap_first_half(g0, g1, cfg: SchemeConfig, bc) -> TwoLevelState:
 
 def _forcing_table(forcing, cfg, grid, parity_src, dt, smax, t0):
     """Host evaluation of the user forcing callable (dissipative.py:102-105):
-    F[s-1][l][t] = h^l dt^s/(l! s!) f(l, s-1, x_t, t0)."""
+    F[s-1][l][t] = h^l dt^s/(l! s!) f(l, s-1, x_t, t0) for every coefficient
+    l < 2m of the velocity interpolant (the reference loops over its full
+    length, dissipative.py:102)."""
     m = cfg.m
-    lv = m
+    lv = 2 * m
     centers = grid.nodes(flip(parity_src))
     h = grid.h
     tab = np.zeros((smax, lv, len(centers)))
