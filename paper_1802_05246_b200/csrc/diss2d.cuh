@@ -299,13 +299,31 @@ template <int P, int PP, int TR>
 __device__ inline void issue_tile(double* __restrict__ dst, const Rows& R, int64_t s_first, int64_t c_first,
                                   const Step2DArgs& a) {
   constexpr int NQ = kTileJ + 1;
+  const bool contiguous = c_first >= 0 && c_first + NQ <= a.ny;
   for (int r = 0; r <= TR; ++r) {
     const RowRef rr = resolve_row(R, s_first + r, a.nx, a.ny * P, a.periodic, a.kxl, a.kxh, 0.0, 0.0);
-    for (int idx = threadIdx.x; idx < NQ * P; idx += blockDim.x) {
-      const int q = idx / P;
-      const int e = idx - q * P;
-      const ColRef cc = resolve_col(c_first + q, a.ny, a.periodic, a.kyl, a.kyh, 0.0, 0.0);
-      cp_async8(dst + (r * NQ + q) * PP + e, rr.p + cc.c * P + e);
+    double* d = dst + r * NQ * PP;
+    if (contiguous) {
+      // interior columns: the row segment is one contiguous block
+      const double* src = rr.p + c_first * P;
+      int q = threadIdx.x / P, e = threadIdx.x - (threadIdx.x / P) * P;
+      const int dq = blockDim.x / P, de = blockDim.x - dq * P;
+      for (int idx = threadIdx.x; idx < NQ * P; idx += blockDim.x) {
+        cp_async8(d + q * PP + e, src + idx);
+        q += dq;
+        e += de;
+        if (e >= P) {
+          e -= P;
+          ++q;
+        }
+      }
+    } else {
+      for (int idx = threadIdx.x; idx < NQ * P; idx += blockDim.x) {
+        const int q = idx / P;
+        const int e = idx - q * P;
+        const ColRef cc = resolve_col(c_first + q, a.ny, a.periodic, a.kyl, a.kyh, 0.0, 0.0);
+        cp_async8(d + q * PP + e, rr.p + cc.c * P + e);
+      }
     }
   }
 }
@@ -404,16 +422,15 @@ __global__ void __launch_bounds__(32 * tile_rows<M>(), M <= 4 ? 2 : 1)
       const double* u1 = u0 + NQ * S::PUP;
       const double* v0 = sv + (warp * NQ + lane) * S::PVP;
       const double* v1 = v0 + NQ * S::PVP;
-      // one class at a time: keeps live ranges (and the i-cache footprint) to one class
-#pragma unroll 1
-      for (int cls = 0; cls < 4; ++cls) {
-        switch (cls) {
-          case 0: diss2d_class<M, 0, 0>(P.t, u0, u1, v0, v1, ou, ov); break;
-          case 1: diss2d_class<M, 0, 1>(P.t, u0, u1, v0, v1, ou, ov); break;
-          case 2: diss2d_class<M, 1, 0>(P.t, u0, u1, v0, v1, ou, ov); break;
-          default: diss2d_class<M, 1, 1>(P.t, u0, u1, v0, v1, ou, ov); break;
-        }
-      }
+      // one class at a time (the __syncwarp fences stop the scheduler from
+      // interleaving classes, which would multiply live registers)
+      diss2d_class<M, 0, 0>(P.t, u0, u1, v0, v1, ou, ov);
+      __syncwarp();
+      diss2d_class<M, 0, 1>(P.t, u0, u1, v0, v1, ou, ov);
+      __syncwarp();
+      diss2d_class<M, 1, 0>(P.t, u0, u1, v0, v1, ou, ov);
+      __syncwarp();
+      diss2d_class<M, 1, 1>(P.t, u0, u1, v0, v1, ou, ov);
     }
     __syncthreads();  // buffer b is refilled by the issue() of the next iteration
     b ^= 1;
