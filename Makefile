@@ -1,20 +1,25 @@
 # Builds the in-tree C-ABI library paper_1802_05246_b200/libhermb200.so for sm_100a.
+# The eight 2D kernel orders live in separate translation units (kern_m*.cu)
+# so `make -j` compiles them in parallel.
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O2 --expt-relaxed-constexpr
+CXXFLAGS := -O2 -fPIC -std=c++17
 SRC := paper_1802_05246_b200/csrc
 LIB := paper_1802_05246_b200/libhermb200.so
-OBJ := build/capi.o build/tables.o
+HDRS := $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.h) include/hermb200.h
+KERN := $(patsubst $(SRC)/%.cu,build/%.o,$(wildcard $(SRC)/kern_m*.cu))
+OBJ := build/capi.o build/tables.o build/cellmap.o $(KERN)
 
 all: $(LIB) tools/fp64_peak
 
-build/capi.o: $(SRC)/capi.cu $(wildcard $(SRC)/*.cuh) $(SRC)/tables.h include/hermb200.h
+build/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) $(PTXAS) -c $< -o $@
 
-build/tables.o: $(SRC)/tables.cpp $(SRC)/tables.h
+build/%.o: $(SRC)/%.cpp $(HDRS)
 	@mkdir -p build
-	g++ -O2 -fPIC -std=c++17 -c $< -o $@
+	g++ $(CXXFLAGS) -c $< -o $@
 
 $(LIB): $(OBJ)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lcudart

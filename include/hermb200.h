@@ -79,6 +79,21 @@ int hw_max_order(void);            /* largest m with a compiled fast path */
 /* interp.py:51-75 interp_matrix(mu): (2mu+2)^2 row-major, exact doubles. */
 int hw_interp_matrix(int mu, double* out_host);
 
+/*
+ * Per-cell linear map of a 2D step (host only; used to pin the kernels'
+ * operator against the reference on the CPU).  scheme: 0 = half_step_2d
+ * (dissipative.py:215-247), 1 = full_step_conservative without the
+ * `- previous` term (conservative.py:130-136), 2 = bootstrap_first_half
+ * (conservative.py:185-195).  hw_cell_map_dims gives din (inputs per corner
+ * node) and dout (outputs per target node); hw_cell_map_2d writes the dense
+ * dout x (4 din) matrix, column = corner * din + e with corner = 2 sx + sy
+ * (sx, sy = 1 for the right / upper neighbour) and e running over the first
+ * input field's (k, l) entries, then the second's.
+ */
+int hw_cell_map_dims(int scheme, int m, int* din, int* dout);
+int hw_cell_map_2d(int scheme, int m, double dt, double hx, double hy, double speed, int stages,
+                   double* out_host);
+
 /* Number of target nodes per axis produced from `n_src` source nodes. */
 int64_t hw_target_count(int64_t n_src, int parity_src, int periodic);
 

@@ -24,7 +24,7 @@ EXPORTS = (
     "hw_last_error", "hw_version", "hw_max_order", "hw_interp_matrix", "hw_target_count",
     "hw_diss2d_half_step", "hw_cons2d_step", "hw_boot2d", "hw_diss1d_half_step",
     "hw_cons1d_step", "hw_boot1d", "hw_l2err2d", "hw_l2err1d", "hw_count_nonfinite",
-    "hw_init_planewave2d", "hw_init_standing2d",
+    "hw_init_planewave2d", "hw_init_standing2d", "hw_cell_map_dims", "hw_cell_map_2d",
 )
 
 
@@ -64,6 +64,8 @@ def _declare(lib):
         "hw_max_order": (_I, []),
         "hw_interp_matrix": (_I, [_I, _P]),
         "hw_target_count": (_L, [_L, _I, _I]),
+        "hw_cell_map_dims": (_I, [_I, _I, C.POINTER(_I), C.POINTER(_I)]),
+        "hw_cell_map_2d": (_I, [_I, _I, _D, _D, _D, _D, _I, _P]),
         "hw_diss2d_half_step": (_I, [C.POINTER(Rows2D), C.POINTER(Rows2D), _P, _P, _I,
                                      C.POINTER(Geom2D), _D, _D, _D, _D, _I, _P]),
         "hw_cons2d_step": (_I, [C.POINTER(Rows2D), _P, _P, _I, C.POINTER(Geom2D),

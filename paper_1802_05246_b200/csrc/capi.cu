@@ -2,20 +2,24 @@
 // construction and kernel dispatch.  Never throws across the ABI.
 #include <cstdio>
 #include <cstring>
+#include <list>
 #include <mutex>
 #include <stdexcept>
 #include <string>
 #include <unordered_map>
 #include <vector>
 
+#include "cellmap.cuh"
+#include "cellmap.h"
 #include "common.cuh"
 #include "diag.cuh"
-#include "diss2d.cuh"
 #include "line1d.cuh"
 #include "tables.h"
-#include "taps2d.cuh"
 
 namespace hw {
+
+template <int M, int SCH>
+cudaError_t launch_cellmap(const CellMapArgs& a, cudaStream_t st);  // kern_m*.cu
 
 static thread_local std::string g_err;
 
@@ -66,135 +70,111 @@ static void check_bc_axis(const hw_axis_bc& b, int periodic) {
            "boundary spec and grid disagree about periodicity");
 }
 
-// phi(a) = a! r^floor(a/2) (dissipative / bootstrap) or a! r^a (conservative)
-static std::vector<double> phi_table(int n, double r, bool full_power) {
-  std::vector<double> p(n);
-  for (int a = 0; a < n; ++a) {
-    const int e = full_power ? a : a / 2;
-    double rp = 1.0;
-    for (int q = 0; q < e; ++q) rp *= r;
-    p[a] = factorial(a) * rp;
+// ------------------------------------------------------------------ cell maps
+// Device copies of the class maps in DMMA fragment order, cached per
+// (device, scheme, m, dt, hx, hy, speed, stages).
+struct DevMap {
+  double* wfrag = nullptr;
+  int* ocode = nullptr;
+  int* icode = nullptr;
+};
+
+struct MapKey {
+  int dev, scheme, m, stages;
+  double dt, hx, hy, speed;
+  bool operator==(const MapKey& o) const {
+    return dev == o.dev && scheme == o.scheme && m == o.m && stages == o.stages &&
+           std::memcmp(&dt, &o.dt, 8) == 0 && std::memcmp(&hx, &o.hx, 8) == 0 &&
+           std::memcmp(&hy, &o.hy, 8) == 0 && std::memcmp(&speed, &o.speed, 8) == 0;
   }
-  return p;
+};
+
+static std::mutex g_map_mu;
+static std::list<std::pair<MapKey, DevMap>> g_maps;  // most recent first
+constexpr size_t kMaxMaps = 48;
+
+static void free_map(DevMap& d) {
+  cudaFree(d.wfrag);
+  cudaFree(d.ocode);
+  cudaFree(d.icode);
 }
 
-// ------------------------------------------------------------------ diss2d
-template <int M>
-static void launch_diss2d(const Step2DArgs& a, double dt, double rx, double ry, int S, cudaStream_t st) {
-  Diss2DParams<M> P;
-  P.a = a;
-  auto& T = P.t;
-  const std::vector<double> hm = hermite_left_block(M);
-  const std::vector<double> hm1 = hermite_left_block(M - 1);
-  const std::vector<double> px = phi_table(2 * M + 2, rx, false);
-  const std::vector<double> py = phi_table(2 * M + 2, ry, false);
-  for (int a2 = 0; a2 < 2 * M + 2; ++a2)
-    for (int k = 0; k <= M; ++k) {
-      T.mx[a2][k] = px[a2] * hm[a2 * (M + 1) + k];
-      T.my[a2][k] = py[a2] * hm[a2 * (M + 1) + k];
+static DevMap device_map(int scheme, int m, double dt, double hx, double hy, double speed, int stages) {
+  MapKey key;
+  std::memset(&key, 0, sizeof(key));
+  cuda_check(cudaGetDevice(&key.dev), "cudaGetDevice");
+  key.scheme = scheme;
+  key.m = m;
+  key.stages = stages;
+  key.dt = dt;
+  key.hx = hx;
+  key.hy = hy;
+  key.speed = speed;
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  for (auto it = g_maps.begin(); it != g_maps.end(); ++it)
+    if (it->first == key) {
+      g_maps.splice(g_maps.begin(), g_maps, it);
+      return g_maps.front().second;
     }
-  for (int a2 = 0; a2 < 2 * M; ++a2)
-    for (int k = 0; k < M; ++k) {
-      T.mx1[a2][k] = px[a2] * hm1[a2 * M + k];
-      T.my1[a2][k] = py[a2] * hm1[a2 * M + k];
-    }
-  const double th = 0.5;
-  for (int i = 0; i < M; ++i)
-    for (int j = 0; j < M; ++j) {
-      const int p = i + j;
-      const double c = binom(p, i);
-      auto pw = [](double x, int e) {
-        double r = 1.0;
-        for (int q = 0; q < e; ++q) r *= x;
-        return r;
-      };
-      T.gA[i][j] = (2 * p + 1 <= S) ? c * pw(th, 2 * p + 1) * pw(dt, p + 1) / factorial(2 * p + 1) : 0.0;
-      T.gB[i][j] = (2 * p + 2 <= S) ? c * pw(th, 2 * p + 2) * pw(dt, p + 1) / factorial(2 * p + 2) : 0.0;
-      T.gG[i][j] = (2 * p <= S) ? c * pw(th, 2 * p) * pw(dt, p) / factorial(2 * p) : 0.0;
-      T.gD[i][j] = (2 * p + 1 <= S) ? c * pw(th, 2 * p + 1) * pw(dt, p) / factorial(2 * p + 1) : 0.0;
-    }
-  for (int k = 0; k <= M; ++k)
-    for (int l = 0; l <= M; ++l) T.inv[k][l] = 1.0 / (px[k] * py[l]);
-
-  const int smem = diss2d_smem_bytes<M>();
-  cuda_check(cudaFuncSetAttribute(diss2d_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-             "cudaFuncSetAttribute(diss2d)");
-  int dev = 0, nsm = 0, per_sm = 0;
-  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-  cuda_check(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "sm count");
-  constexpr int TR = tile_rows<M>();
-  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, diss2d_kernel<M>, 32 * TR, smem), "occupancy");
-  const int64_t ntiles = ((a.nty + kTileJ - 1) / kTileJ) * ((a.ntrows + TR - 1) / TR);
-  int64_t nblk = (int64_t)nsm * (per_sm > 0 ? per_sm : 1);
-  if (nblk > ntiles) nblk = ntiles;
-  diss2d_kernel<M><<<(unsigned)nblk, 32 * TR, smem, st>>>(P);
-  cuda_check(cudaGetLastError(), "diss2d launch");
+  const CellMap cm = build_cell_map(scheme, m, dt, hx, hy, speed, stages);
+  const int nk = cm_nk(scheme, m), nt = cm_nt(scheme, m);
+  std::vector<double> wf((size_t)nk * nt * 32, 0.0);
+  std::vector<int> oc((size_t)nt * 8, -1), ic((size_t)nk * 4, 0);
+  const int p0 = cm.w_in[0] * cm.w_in[0];
+  for (int e = 0; e < cm.din; ++e) {
+    const int w = e < p0 ? cm.w_in[0] : cm.w_in[1];
+    const int ee = e < p0 ? e : e - p0;
+    ic[e] = ((ee / w) & 1) | (((ee % w) & 1) << 1);
+  }
+  for (int c = 0; c < 4; ++c) {
+    if (cm.ncls[c] != cm_ncls(scheme, m, c)) throw Error(HW_EINVAL, "internal: class size mismatch");
+    const int base = cm_ntbase(scheme, m, c);
+    for (int o = 0; o < cm.ncls[c]; ++o) oc[(size_t)(base + o / 8) * 8 + o % 8] = cm.code[c][o];
+    for (int ks = 0; ks < nk; ++ks)
+      for (int j = 0; j < cm_ntc(scheme, m, c); ++j)
+        for (int lane = 0; lane < 32; ++lane) {
+          const int o = 8 * j + lane / 4, e = 4 * ks + lane % 4;
+          if (o < cm.ncls[c] && e < cm.din)
+            wf[((size_t)ks * nt + base + j) * 32 + lane] = cm.w[c][(size_t)o * cm.din + e];
+        }
+  }
+  DevMap d;
+  try {
+    cuda_check(cudaMalloc(&d.wfrag, wf.size() * sizeof(double)), "cudaMalloc(wfrag)");
+    cuda_check(cudaMalloc(&d.ocode, oc.size() * sizeof(int)), "cudaMalloc(ocode)");
+    cuda_check(cudaMalloc(&d.icode, ic.size() * sizeof(int)), "cudaMalloc(icode)");
+    cuda_check(cudaMemcpy(d.wfrag, wf.data(), wf.size() * sizeof(double), cudaMemcpyHostToDevice), "upload wfrag");
+    cuda_check(cudaMemcpy(d.ocode, oc.data(), oc.size() * sizeof(int), cudaMemcpyHostToDevice), "upload ocode");
+    cuda_check(cudaMemcpy(d.icode, ic.data(), ic.size() * sizeof(int), cudaMemcpyHostToDevice), "upload icode");
+  } catch (...) {
+    free_map(d);
+    throw;
+  }
+  if (g_maps.size() >= kMaxMaps) {
+    cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+    free_map(g_maps.back().second);
+    g_maps.pop_back();
+  }
+  g_maps.emplace_front(key, d);
+  return d;
 }
 
-// ------------------------------------------------------------------ taps2d
-template <int M, int NIN>
-static void launch_taps2d(const Taps2DArgs& a, const std::vector<double>& px, const std::vector<double>& py,
-                          const std::vector<std::vector<double>>& g, double scale, cudaStream_t st) {
-  Taps2DParams<M, NIN> P;
-  P.a = a;
-  auto& T = P.t;
-  const std::vector<double> hm = hermite_left_block(M);
-  for (int a2 = 0; a2 < 2 * M + 2; ++a2)
-    for (int k = 0; k <= M; ++k) {
-      T.mx[a2][k] = px[a2] * hm[a2 * (M + 1) + k];
-      T.my[a2][k] = py[a2] * hm[a2 * (M + 1) + k];
-    }
-  for (int f = 0; f < NIN; ++f)
-    for (int i = 0; i <= M; ++i)
-      for (int j = 0; j <= M; ++j) T.g[f][i][j] = g[f][i * (M + 1) + j];
-  for (int k = 0; k <= M; ++k)
-    for (int l = 0; l <= M; ++l) T.inv[k][l] = scale / (px[k] * py[l]);
-  using S_ = Taps2DSmem<M>;
-  const int smem = (NIN * 2 * S_::NQ * S_::PP + kTileJ * S_::P) * 8;
-  cuda_check(cudaFuncSetAttribute(taps2d_kernel<M, NIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-             "cudaFuncSetAttribute(taps2d)");
-  const int64_t nct = (a.nty + kTileJ - 1) / kTileJ;
-  const int64_t gy = a.ntrows < 65535 ? a.ntrows : 65535;
-  dim3 grid((unsigned)nct, (unsigned)gy);
-  taps2d_kernel<M, NIN><<<grid, 128, smem, st>>>(P);
-  cuda_check(cudaGetLastError(), "taps2d launch");
-}
-
-template <template <int> class F, class... A>
-static void dispatch_m(int m, A&&... args) {
+template <int SCH>
+static void dispatch_cellmap(int m, const CellMapArgs& a, cudaStream_t st) {
+  cudaError_t e;
   switch (m) {
-    case 1: F<1>::run(args...); break;
-    case 2: F<2>::run(args...); break;
-    case 3: F<3>::run(args...); break;
-    case 4: F<4>::run(args...); break;
-    case 5: F<5>::run(args...); break;
-    case 6: F<6>::run(args...); break;
-    case 7: F<7>::run(args...); break;
-    case 8: F<8>::run(args...); break;
+    case 1: e = launch_cellmap<1, SCH>(a, st); break;
+    case 2: e = launch_cellmap<2, SCH>(a, st); break;
+    case 3: e = launch_cellmap<3, SCH>(a, st); break;
+    case 4: e = launch_cellmap<4, SCH>(a, st); break;
+    case 5: e = launch_cellmap<5, SCH>(a, st); break;
+    case 6: e = launch_cellmap<6, SCH>(a, st); break;
+    case 7: e = launch_cellmap<7, SCH>(a, st); break;
+    case 8: e = launch_cellmap<8, SCH>(a, st); break;
     default: throw Error(HW_EUNSUPPORTED, "method order m=" + std::to_string(m) + " has no compiled 2D path (1..8)");
   }
+  cuda_check(e, "cellmap launch");
 }
-
-template <int M>
-struct Diss2DRun {
-  static void run(const Step2DArgs& a, double dt, double rx, double ry, int S, cudaStream_t st) {
-    launch_diss2d<M>(a, dt, rx, ry, S, st);
-  }
-};
-template <int M>
-struct ConsRun {
-  static void run(const Taps2DArgs& a, const std::vector<double>& px, const std::vector<double>& py,
-                  const std::vector<std::vector<double>>& g, double scale, cudaStream_t st) {
-    launch_taps2d<M, 1>(a, px, py, g, scale, st);
-  }
-};
-template <int M>
-struct BootRun {
-  static void run(const Taps2DArgs& a, const std::vector<double>& px, const std::vector<double>& py,
-                  const std::vector<std::vector<double>>& g, double scale, cudaStream_t st) {
-    launch_taps2d<M, 2>(a, px, py, g, scale, st);
-  }
-};
 
 struct Geo {
   int64_t nx, ny, ntx, nty, trow0, ntrows;
@@ -221,72 +201,15 @@ static Geo check_geom(const hw_geom2d* g) {
   return o;
 }
 
-}  // namespace hw
-
-using namespace hw;
-
-extern "C" {
-
-const char* hw_last_error(void) { return g_err.c_str(); }
-int hw_version(void) { return 1; }
-int hw_max_order(void) { return kMaxFast; }
-
-int hw_interp_matrix(int mu, double* out) {
-  return guard([&] {
-    HW_CHECK(out, "null output");
-    HW_CHECK(mu >= 0 && mu <= kMaxOrder, "interpolation order must be in [0, 12]");
-    const std::vector<double> m = hermite_matrix(mu);
-    std::memcpy(out, m.data(), m.size() * sizeof(double));
-  });
-}
-
-int64_t hw_target_count(int64_t n_src, int parity_src, int periodic) {
-  return target_count(n_src, parity_src, periodic);
-}
-
-int hw_diss2d_half_step(const hw_rows2d* u_src, const hw_rows2d* v_src, double* u_dst, double* v_dst, int m,
-                        const hw_geom2d* geom, double dt, double hx, double hy, double speed, int stage_cap,
-                        void* stream) {
-  return guard([&] {
-    HW_CHECK(u_src && v_src && u_src->base && v_src->base && u_dst && v_dst, "null field pointer");
-    HW_CHECK(m >= 1, "method order must be >= 1");
-    const Geo g = check_geom(geom);
-    if (g.ntrows == 0) return;
-    Step2DArgs a;
-    a.u = to_rows(u_src);
-    a.v = to_rows(v_src);
-    a.ud = u_dst;
-    a.vd = v_dst;
-    a.nx = g.nx;
-    a.ny = g.ny;
-    a.trow0 = g.trow0;
-    a.ntrows = g.ntrows;
-    a.nty = g.nty;
-    a.off = g.off;
-    a.periodic = g.periodic;
-    a.kxl = g.periodic ? 0 : geom->bcx.left_kind;
-    a.kxh = g.periodic ? 0 : geom->bcx.right_kind;
-    a.kyl = g.periodic ? 0 : geom->bcy.left_kind;
-    a.kyh = g.periodic ? 0 : geom->bcy.right_kind;
-    a.gxl = geom->bcx.left_value;
-    a.gxh = geom->bcx.right_value;
-    a.gyl = geom->bcy.left_value;
-    a.gyh = geom->bcy.right_value;
-    // dissipative.py:227,234-235 (rx, ry exactly as the reference forms them)
-    const double rx = speed * speed * dt / (hx * hx);
-    const double ry = speed * speed * dt / (hy * hy);
-    const int S = stage_cap > 0 ? stage_cap : 4 * m + 4;
-    dispatch_m<Diss2DRun>(m, a, dt, rx, ry, S, (cudaStream_t)stream);
-  });
-}
-
-static Taps2DArgs taps_args(const Geo& g, const hw_geom2d* geom, const hw_rows2d* f0, const hw_rows2d* f1,
-                            const double* prev, double* out) {
-  Taps2DArgs a;
+static CellMapArgs cellmap_args(const Geo& g, const hw_geom2d* geom, const hw_rows2d* f0, const hw_rows2d* f1,
+                                const DevMap& dm) {
+  CellMapArgs a;
+  std::memset(&a, 0, sizeof(a));
   a.f0 = to_rows(f0);
   a.f1 = f1 ? to_rows(f1) : a.f0;
-  a.prev = prev;
-  a.out = out;
+  a.wfrag = dm.wfrag;
+  a.ocode = dm.ocode;
+  a.icode = dm.icode;
   a.nx = g.nx;
   a.ny = g.ny;
   a.trow0 = g.trow0;
@@ -302,8 +225,76 @@ static Taps2DArgs taps_args(const Geo& g, const hw_geom2d* geom, const hw_rows2d
   a.gxh = geom->bcx.right_value;
   a.gyl = geom->bcy.left_value;
   a.gyh = geom->bcy.right_value;
-  a.g1scale = 0.0;
   return a;
+}
+
+static void check_rows(const hw_rows2d* r, const Geo& g) {
+  HW_CHECK(r->nrows >= 0 && r->row0 >= 0 && r->row0 + r->nrows <= g.nx, "source row window out of bounds");
+}
+
+}  // namespace hw
+
+using namespace hw;
+
+extern "C" {
+
+const char* hw_last_error(void) { return g_err.c_str(); }
+int hw_version(void) { return 2; }
+int hw_max_order(void) { return kMaxFast; }
+
+int hw_interp_matrix(int mu, double* out) {
+  return guard([&] {
+    HW_CHECK(out, "null output");
+    HW_CHECK(mu >= 0 && mu <= kMaxOrder, "interpolation order must be in [0, 12]");
+    const std::vector<double> m = hermite_matrix(mu);
+    std::memcpy(out, m.data(), m.size() * sizeof(double));
+  });
+}
+
+int64_t hw_target_count(int64_t n_src, int parity_src, int periodic) {
+  return target_count(n_src, parity_src, periodic);
+}
+
+int hw_cell_map_dims(int scheme, int m, int* din, int* dout) {
+  return guard([&] {
+    HW_CHECK(din && dout, "null output");
+    HW_CHECK(scheme >= kDiss && scheme <= kBoot, "unknown scheme");
+    HW_CHECK(m >= 1 && m <= kMaxOrder - 1, "method order out of range");
+    *din = cm_din(scheme, m);
+    *dout = cm_dout(scheme, m);
+  });
+}
+
+int hw_cell_map_2d(int scheme, int m, double dt, double hx, double hy, double speed, int stages, double* out) {
+  return guard([&] {
+    HW_CHECK(out, "null output");
+    HW_CHECK(scheme >= kDiss && scheme <= kBoot, "unknown scheme");
+    HW_CHECK(m >= 1 && m <= kMaxOrder - 1, "method order out of range");
+    HW_CHECK(stages >= 1 || scheme == kCons, "stage count must be >= 1");
+    const CellMap cm = build_cell_map(scheme, m, dt, hx, hy, speed, stages);
+    const std::vector<double> d = dense_cell_map(cm);
+    std::memcpy(out, d.data(), d.size() * sizeof(double));
+  });
+}
+
+int hw_diss2d_half_step(const hw_rows2d* u_src, const hw_rows2d* v_src, double* u_dst, double* v_dst, int m,
+                        const hw_geom2d* geom, double dt, double hx, double hy, double speed, int stage_cap,
+                        void* stream) {
+  return guard([&] {
+    HW_CHECK(u_src && v_src && u_src->base && v_src->base && u_dst && v_dst, "null field pointer");
+    HW_CHECK(m >= 1, "method order must be >= 1");
+    const Geo g = check_geom(geom);
+    check_rows(u_src, g);
+    check_rows(v_src, g);
+    if (g.ntrows == 0) return;
+    const int S = stage_cap > 0 ? stage_cap : 4 * m + 4;  // dissipative.py:73-74
+    HW_CHECK(m <= kMaxFast, "method order m=" + std::to_string(m) + " has no compiled 2D path (1..8)");
+    const DevMap dm = device_map(kDiss, m, dt, hx, hy, speed, S);
+    CellMapArgs a = cellmap_args(g, geom, u_src, v_src, dm);
+    a.out0 = u_dst;
+    a.out1 = v_dst;
+    dispatch_cellmap<kDiss>(m, a, (cudaStream_t)stream);
+  });
 }
 
 int hw_cons2d_step(const hw_rows2d* cur_src, const double* prev, double* out, int m, const hw_geom2d* geom,
@@ -312,16 +303,14 @@ int hw_cons2d_step(const hw_rows2d* cur_src, const double* prev, double* out, in
     HW_CHECK(cur_src && cur_src->base && prev && out, "null field pointer");
     HW_CHECK(m >= 1, "method order must be >= 1");
     const Geo g = check_geom(geom);
+    check_rows(cur_src, g);
     if (g.ntrows == 0) return;
-    Taps2DArgs a = taps_args(g, geom, cur_src, nullptr, prev, out);
-    // conservative.py:133-136: rho = c dt / (2h) per axis
-    const double rhox = 0.5 * speed * dt / hx, rhoy = 0.5 * speed * dt / hy;
-    const int K = 2 * m + 2;
-    std::vector<double> px = phi_table(K, rhox, true), py = phi_table(K, rhoy, true);
-    std::vector<std::vector<double>> gt(1, std::vector<double>((size_t)(m + 1) * (m + 1)));
-    for (int i = 0; i <= m; ++i)
-      for (int j = 0; j <= m; ++j) gt[0][i * (m + 1) + j] = binom(i + j, i) / factorial(2 * i + 2 * j);
-    dispatch_m<ConsRun>(m, a, px, py, gt, 2.0, (cudaStream_t)stream);
+    HW_CHECK(m <= kMaxFast, "method order m=" + std::to_string(m) + " has no compiled 2D path (1..8)");
+    const DevMap dm = device_map(kCons, m, dt, hx, hy, speed, 0);
+    CellMapArgs a = cellmap_args(g, geom, cur_src, nullptr, dm);
+    a.prev = prev;
+    a.out0 = out;
+    dispatch_cellmap<kCons>(m, a, (cudaStream_t)stream);
   });
 }
 
@@ -331,24 +320,14 @@ int hw_boot2d(const hw_rows2d* g0_src, const hw_rows2d* g1_src, double* out, int
     HW_CHECK(g0_src && g1_src && g0_src->base && g1_src->base && out, "null field pointer");
     HW_CHECK(m >= 1, "method order must be >= 1");
     const Geo g = check_geom(geom);
+    check_rows(g0_src, g);
+    check_rows(g1_src, g);
     if (g.ntrows == 0) return;
-    Taps2DArgs a = taps_args(g, geom, g0_src, g1_src, nullptr, out);
-    const double rx = speed * speed * dt / (hx * hx), ry = speed * speed * dt / (hy * hy);
-    const int K = 2 * m + 2;
-    std::vector<double> px = phi_table(K, rx, false), py = phi_table(K, ry, false);
-    std::vector<std::vector<double>> gt(2, std::vector<double>((size_t)(m + 1) * (m + 1)));
-    const double th = 0.5;
-    const int S = 4 * m + 4;  // conservative.py:192
-    for (int i = 0; i <= m; ++i)
-      for (int j = 0; j <= m; ++j) {
-        const int p = i + j;
-        double thp = 1.0, dtp = 1.0;
-        for (int q = 0; q < 2 * p; ++q) thp *= th;
-        for (int q = 0; q < p; ++q) dtp *= dt;
-        gt[0][i * (m + 1) + j] = (2 * p <= S) ? binom(p, i) * thp * dtp / factorial(2 * p) : 0.0;
-        gt[1][i * (m + 1) + j] = (2 * p + 1 <= S) ? binom(p, i) * thp * th * dtp * dt / factorial(2 * p + 1) : 0.0;
-      }
-    dispatch_m<BootRun>(m, a, px, py, gt, 1.0, (cudaStream_t)stream);
+    HW_CHECK(m <= kMaxFast, "method order m=" + std::to_string(m) + " has no compiled 2D path (1..8)");
+    const DevMap dm = device_map(kBoot, m, dt, hx, hy, speed, 4 * m + 4);  // conservative.py:192
+    CellMapArgs a = cellmap_args(g, geom, g0_src, g1_src, dm);
+    a.out0 = out;
+    dispatch_cellmap<kBoot>(m, a, (cudaStream_t)stream);
   });
 }
 

@@ -1,0 +1,37 @@
+// Launcher of cellmap_kernel<M, SCH>; instantiated per order in kern_m*.cu so
+// the eight orders compile in parallel.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "cellmap.cuh"
+
+namespace hw {
+
+// Persistent grid: one wave of CTAs (SM count x resident CTAs per SM).
+template <int M, int SCH>
+cudaError_t launch_cellmap(const CellMapArgs& a, cudaStream_t st) {
+  using C = CMCfg<M, SCH>;
+  static_assert(C::SMEM <= 227 * 1024, "stage ring exceeds the 227 KB shared-memory limit");
+  auto kern = cellmap_kernel<M, SCH>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  if (e != cudaSuccess) return e;
+  int dev = 0, nsm = 0, per_sm = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * C::NW, C::SMEM)) != cudaSuccess)
+    return e;
+  const int64_t ntiles = ((a.nty + C::TJ - 1) / C::TJ) * ((a.ntrows + C::TR - 1) / C::TR);
+  int64_t nblk = (int64_t)nsm * (per_sm > 0 ? per_sm : 1);
+  if (nblk > ntiles) nblk = ntiles;
+  if (nblk <= 0) return cudaSuccess;
+  kern<<<(unsigned)nblk, 32 * C::NW, C::SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
+#define HW_INSTANTIATE_CELLMAP(M)                                                   \
+  template cudaError_t launch_cellmap<M, kDiss>(const CellMapArgs&, cudaStream_t); \
+  template cudaError_t launch_cellmap<M, kCons>(const CellMapArgs&, cudaStream_t); \
+  template cudaError_t launch_cellmap<M, kBoot>(const CellMapArgs&, cudaStream_t);
+
+}  // namespace hw

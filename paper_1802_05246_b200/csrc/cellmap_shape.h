@@ -1,0 +1,43 @@
+// Compile-time shape of the per-class cell maps (shared by the host builder
+// and the sm_100a kernel so both agree on the class/tile layout).
+#pragma once
+
+namespace hw {
+
+enum Scheme : int { kDiss = 0, kCons = 1, kBoot = 2 };
+
+// field widths (orders + 1) of the inputs / outputs of each scheme
+constexpr int cm_win(int sch, int m, int f) { return f == 0 ? m + 1 : (sch == 0 ? m : (sch == 2 ? m + 1 : 0)); }
+constexpr int cm_wout(int sch, int m, int f) { return f == 0 ? m + 1 : (sch == 0 ? m : 0); }
+
+// number of k in [0, w) with k % 2 == p
+constexpr int cm_cnt_par(int w, int p) { return w > p ? (w - 1 - p) / 2 + 1 : 0; }
+
+constexpr int cm_din(int sch, int m) { return cm_win(sch, m, 0) * cm_win(sch, m, 0) + cm_win(sch, m, 1) * cm_win(sch, m, 1); }
+constexpr int cm_dout(int sch, int m) {
+  return cm_wout(sch, m, 0) * cm_wout(sch, m, 0) + cm_wout(sch, m, 1) * cm_wout(sch, m, 1);
+}
+
+// outputs of parity class c = (PA, PB) = (c >> 1, c & 1)
+constexpr int cm_ncls(int sch, int m, int c) {
+  return cm_cnt_par(cm_wout(sch, m, 0), c >> 1) * cm_cnt_par(cm_wout(sch, m, 0), c & 1) +
+         cm_cnt_par(cm_wout(sch, m, 1), c >> 1) * cm_cnt_par(cm_wout(sch, m, 1), c & 1);
+}
+
+// 8-wide output tiles of class c (DMMA m8n8k4: N = 8) and their prefix sums
+constexpr int cm_ntc(int sch, int m, int c) { return (cm_ncls(sch, m, c) + 7) / 8; }
+constexpr int cm_ntbase(int sch, int m, int c) {  // non-recursive: folds inside unrolled device loops
+  return (c > 0 ? cm_ntc(sch, m, 0) : 0) + (c > 1 ? cm_ntc(sch, m, 1) : 0) + (c > 2 ? cm_ntc(sch, m, 2) : 0) +
+         (c > 3 ? cm_ntc(sch, m, 3) : 0);
+}
+constexpr int cm_nt(int sch, int m) { return cm_ntbase(sch, m, 4); }
+
+// parity class that output tile nt belongs to
+constexpr int cm_class_of_tile(int sch, int m, int nt) {
+  return nt < cm_ntbase(sch, m, 1) ? 0 : (nt < cm_ntbase(sch, m, 2) ? 1 : (nt < cm_ntbase(sch, m, 3) ? 2 : 3));
+}
+
+// 4-deep input steps (DMMA K = 4)
+constexpr int cm_nk(int sch, int m) { return (cm_din(sch, m) + 3) / 4; }
+
+}  // namespace hw

@@ -1,0 +1,6 @@
+// Instantiates the fused 2D cell-map kernels for method order m = 4.
+#include "cellmap_launch.cuh"
+
+namespace hw {
+HW_INSTANTIATE_CELLMAP(4)
+}  // namespace hw

@@ -1,0 +1,6 @@
+// Instantiates the fused 2D cell-map kernels for method order m = 7.
+#include "cellmap_launch.cuh"
+
+namespace hw {
+HW_INSTANTIATE_CELLMAP(7)
+}  // namespace hw
