@@ -120,21 +120,30 @@ static DevMap device_map(int scheme, int m, double dt, double hx, double hy, dou
   const int nk = cm_nk(scheme, m), nt = cm_nt(scheme, m);
   std::vector<double> wf((size_t)nk * nt * 32, 0.0);
   std::vector<int> oc((size_t)nt * 8, -1), ic((size_t)nk * 4, 0);
-  const int p0 = cm.w_in[0] * cm.w_in[0];
-  for (int e = 0; e < cm.din; ++e) {
-    const int w = e < p0 ? cm.w_in[0] : cm.w_in[1];
-    const int ee = e < p0 ? e : e - p0;
-    ic[e] = ((ee / w) & 1) | (((ee % w) & 1) << 1);
+  // input slot -> map input e (field 0 entries, then field 1); -1 = pad slot
+  const int p0 = cm.w_in[0] * cm.w_in[0], p1 = cm.w_in[1] * cm.w_in[1], k0 = cm_k0(scheme, m);
+  std::vector<int> slot_e((size_t)nk * 4, -1);
+  for (int sl = 0; sl < nk * 4; ++sl) {
+    const bool f1 = sl >= k0;
+    const int ee = f1 ? sl - k0 : sl;
+    if (ee >= (f1 ? p1 : p0)) continue;
+    const int w = cm.w_in[f1 ? 1 : 0];
+    slot_e[sl] = f1 ? p0 + ee : ee;
+    ic[sl] = ((ee / w) & 1) | (((ee % w) & 1) << 1);
   }
   for (int c = 0; c < 4; ++c) {
     if (cm.ncls[c] != cm_ncls(scheme, m, c)) throw Error(HW_EINVAL, "internal: class size mismatch");
     const int base = cm_ntbase(scheme, m, c);
-    for (int o = 0; o < cm.ncls[c]; ++o) oc[(size_t)(base + o / 8) * 8 + o % 8] = cm.code[c][o];
+    const int o0 = cm.w_out[0] * cm.w_out[0];
+    for (int o = 0; o < cm.ncls[c]; ++o) {  // position in the [field 0 | field 1] output record
+      const int code = cm.code[c][o];
+      oc[(size_t)(base + o / 8) * 8 + o % 8] = (code >> 16 ? o0 : 0) + (code & 0xffff);
+    }
     for (int ks = 0; ks < nk; ++ks)
       for (int j = 0; j < cm_ntc(scheme, m, c); ++j)
         for (int lane = 0; lane < 32; ++lane) {
-          const int o = 8 * j + lane / 4, e = 4 * ks + lane % 4;
-          if (o < cm.ncls[c] && e < cm.din)
+          const int o = 8 * j + lane / 4, e = slot_e[4 * ks + lane % 4];
+          if (o < cm.ncls[c] && e >= 0)
             wf[((size_t)ks * nt + base + j) * 32 + lane] = cm.w[c][(size_t)o * cm.din + e];
         }
   }
@@ -202,7 +211,9 @@ static Geo check_geom(const hw_geom2d* g) {
 }
 
 static CellMapArgs cellmap_args(const Geo& g, const hw_geom2d* geom, const hw_rows2d* f0, const hw_rows2d* f1,
-                                const DevMap& dm) {
+                                const DevMap& dm, int m) {
+  // the kernel stages with 32-bit offsets within a source row
+  HW_CHECK(g.ny * (int64_t)(m + 1) * (m + 1) < ((int64_t)1 << 31), "grid row too long for the 2D kernels");
   CellMapArgs a;
   std::memset(&a, 0, sizeof(a));
   a.f0 = to_rows(f0);
@@ -228,8 +239,10 @@ static CellMapArgs cellmap_args(const Geo& g, const hw_geom2d* geom, const hw_ro
   return a;
 }
 
-static void check_rows(const hw_rows2d* r, const Geo& g) {
+static void check_rows(const hw_rows2d* r, const Geo& g, const hw_rows2d* first = nullptr) {
   HW_CHECK(r->nrows >= 0 && r->row0 >= 0 && r->row0 + r->nrows <= g.nx, "source row window out of bounds");
+  HW_CHECK(!first || (first->row0 == r->row0 && first->nrows == r->nrows),
+           "both source fields must cover the same row window");
 }
 
 }  // namespace hw
@@ -285,12 +298,12 @@ int hw_diss2d_half_step(const hw_rows2d* u_src, const hw_rows2d* v_src, double* 
     HW_CHECK(m >= 1, "method order must be >= 1");
     const Geo g = check_geom(geom);
     check_rows(u_src, g);
-    check_rows(v_src, g);
+    check_rows(v_src, g, u_src);
     if (g.ntrows == 0) return;
     const int S = stage_cap > 0 ? stage_cap : 4 * m + 4;  // dissipative.py:73-74
     HW_CHECK(m <= kMaxFast, "method order m=" + std::to_string(m) + " has no compiled 2D path (1..8)");
     const DevMap dm = device_map(kDiss, m, dt, hx, hy, speed, S);
-    CellMapArgs a = cellmap_args(g, geom, u_src, v_src, dm);
+    CellMapArgs a = cellmap_args(g, geom, u_src, v_src, dm, m);
     a.out0 = u_dst;
     a.out1 = v_dst;
     dispatch_cellmap<kDiss>(m, a, (cudaStream_t)stream);
@@ -307,7 +320,7 @@ int hw_cons2d_step(const hw_rows2d* cur_src, const double* prev, double* out, in
     if (g.ntrows == 0) return;
     HW_CHECK(m <= kMaxFast, "method order m=" + std::to_string(m) + " has no compiled 2D path (1..8)");
     const DevMap dm = device_map(kCons, m, dt, hx, hy, speed, 0);
-    CellMapArgs a = cellmap_args(g, geom, cur_src, nullptr, dm);
+    CellMapArgs a = cellmap_args(g, geom, cur_src, nullptr, dm, m);
     a.prev = prev;
     a.out0 = out;
     dispatch_cellmap<kCons>(m, a, (cudaStream_t)stream);
@@ -321,11 +334,11 @@ int hw_boot2d(const hw_rows2d* g0_src, const hw_rows2d* g1_src, double* out, int
     HW_CHECK(m >= 1, "method order must be >= 1");
     const Geo g = check_geom(geom);
     check_rows(g0_src, g);
-    check_rows(g1_src, g);
+    check_rows(g1_src, g, g0_src);
     if (g.ntrows == 0) return;
     HW_CHECK(m <= kMaxFast, "method order m=" + std::to_string(m) + " has no compiled 2D path (1..8)");
     const DevMap dm = device_map(kBoot, m, dt, hx, hy, speed, 4 * m + 4);  // conservative.py:192
-    CellMapArgs a = cellmap_args(g, geom, g0_src, g1_src, dm);
+    CellMapArgs a = cellmap_args(g, geom, g0_src, g1_src, dm, m);
     a.out0 = out;
     dispatch_cellmap<kBoot>(m, a, (cudaStream_t)stream);
   });

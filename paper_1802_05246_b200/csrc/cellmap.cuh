@@ -11,12 +11,14 @@
 // the four classes' G at once; the B operand (W, pre-arranged on the host in
 // fragment order) is read conflict-free from shared memory.
 //
-// Data movement: persistent CTAs walk tiles of TR x TJ target cells.  Each
-// tile is consumed in K-chunks of 16 inputs; a chunk stages the
-// (TR+1) x (TJ+1) source nodes' 16 entries plus the matching 4 k-steps of W
-// with cp.async into an NS-deep ring, so the loads of chunk g+2 overlap the
-// tensor-core work of chunk g.  Accumulators live in registers for the whole
-// tile; the epilogue stores them straight to the output records.
+// Warp specialisation.  Four producer warps stage, for every (tile, K-chunk)
+// of the CTA's persistent tile sequence, the 16-entry slices of the tile's
+// (TR+1) x (TJ+1) source nodes plus the chunk's W fragments into an NS-deep
+// shared-memory ring with cp.async; completion is tracked by mbarriers
+// (cp.async.mbarrier.arrive), never by a CTA-wide barrier.  Eight consumer
+// warps wait on the ring's `full` barriers, run the DMMAs and release the slot
+// on its `empty` barrier, so consumers drift freely relative to each other and
+// the epilogue of one warp overlaps the tensor-core work of the others.
 #pragma once
 
 #include <stdint.h>
@@ -29,8 +31,8 @@ namespace hw {
 struct CellMapArgs {
   Rows f0, f1;                 // source fields (f1 unused when the scheme has one input)
   const double* wfrag;         // [NK][NT][32] B fragments
-  const int* ocode;            // [NT][8] field << 16 | offset, -1 = padding
-  const int* icode;            // [NK*4] (kx & 1) | (ky & 1) << 1 of each input entry
+  const int* ocode;            // [NT][8] position in the cell's [field 0 | field 1] output record, -1 = padding
+  const int* icode;            // [NK*4] (kx & 1) | (ky & 1) << 1 of each input slot
   const double* prev;          // kCons: previous level (may alias out0)
   double* out0;
   double* out1;
@@ -44,45 +46,69 @@ struct CellMapArgs {
 template <int M, int SCH>
 struct CMCfg {
   static constexpr int W0 = cm_win(SCH, M, 0), W1 = cm_win(SCH, M, 1);
-  static constexpr int P0 = W0 * W0, P1 = W1 * W1, DIN = P0 + P1;
+  static constexpr int P0 = W0 * W0, P1 = W1 * W1;
+  static constexpr int K0 = cm_k0(SCH, M);        // input slots of field 0 (P0 rounded up to 4)
   static constexpr int O0 = cm_wout(SCH, M, 0) * cm_wout(SCH, M, 0);
   static constexpr int O1 = cm_wout(SCH, M, 1) * cm_wout(SCH, M, 1);
   static constexpr int NK = cm_nk(SCH, M), NT = cm_nt(SCH, M);
   static constexpr int B1 = cm_ntbase(SCH, M, 1), B2 = cm_ntbase(SCH, M, 2), B3 = cm_ntbase(SCH, M, 3);
   static constexpr int KSC = 4;                    // k-steps per chunk
-  static constexpr int KC = 4 * KSC;               // inputs per chunk
+  static constexpr int KC = 4 * KSC;               // input slots per chunk
   static constexpr int NCH = (NK + KSC - 1) / KSC; // chunks per tile
   static constexpr int KCP = 20;                   // staged doubles per node (= 4 mod 16: conflict-free)
-  // Tile and warp shape by accumulator footprint (MT x NT x 2 doubles per
-  // thread): small maps give each warp two M-tiles (each W fragment feeds two
-  // DMMAs) at two CTAs per SM; large maps one M-tile per warp at one CTA.
-  static constexpr bool BIG = NT > 7;
-  static constexpr int MT = BIG ? 1 : 2;           // 8-cell M-tiles per warp
-  static constexpr int NW = 8;                     // warps per CTA
+  // 8-cell M-tiles per consumer warp: two (each W fragment feeds two DMMAs)
+  // while the accumulators fit the 168-register budget of 3 warps per SMSP
+  static constexpr int MT = NT <= 9 ? 2 : 1;
+  static constexpr int NW = 8;                     // consumer warps
+  static constexpr int NPW = 4;                    // producer warps (one per SM sub-partition)
+  static constexpr int NTHREADS = 32 * (NW + NPW);
   static constexpr int TJ = 32;                    // target columns per tile
   static constexpr int TR = NW * MT / (TJ / 8);    // target rows per tile
   static constexpr int NODES = (TR + 1) * (TJ + 1);
   static constexpr int CBUF = NODES * KCP;
   static constexpr int WBUF = KSC * NT * 32;
-  static constexpr int SBUF = CBUF + WBUF;         // doubles per pipeline stage
-  static constexpr int NS = 3;                     // pipeline depth
-  static constexpr int SMEM = NS * SBUF * 8 + (NK * 4 + NT * 8) * 4;
-  static constexpr int MINB = 1;                   // CTAs per SM the register budget targets
-  static constexpr bool UNROLL_KS = !BIG;          // software-pipeline the k-steps of a chunk
+  static constexpr int SBUF = CBUF + WBUF;         // doubles per ring slot
+  static constexpr int DO = O0 + O1;               // output record per cell
+  static constexpr int EPIB = NW * 8 * DO;         // per-warp epilogue staging (doubles)
+  static constexpr int TAIL = EPIB * 8 + NT * 8 * 4 + 64;
+  static constexpr int NS = (4 * SBUF * 8 + TAIL <= 227 * 1024) ? 4 : 3;  // ring depth
+  static constexpr int EPI0 = NS * SBUF;           // double offset of the staging slabs
+  static constexpr int SMEM = NS * SBUF * 8 + TAIL;
+  static constexpr bool UNROLL_KS = NT <= 9;       // fully unroll the k-steps of a chunk
 };
 
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
 __device__ __forceinline__ void cm_cp_async8(double* dst, const double* src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cm_cp_async16(double* dst, const double* src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
-__device__ __forceinline__ void cm_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cm_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+
+// mbarrier primitives (CTA scope).
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+// Arrive once all of this thread's prior cp.async copies have landed.
+__device__ __forceinline__ void mbar_arrive_cp_async(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
 }
 
 // D += A B on the FP64 tensor cores (one 8x8x4 tile per warp).
@@ -97,10 +123,8 @@ __device__ __forceinline__ double flip_sign(double x, unsigned long long mask) {
 }
 
 // Source row s of a field: local rows, slab halos, periodic wrap, wall ghost
-// (boundary.py:119-130).  kind = wall kind of a ghost row, else 0.
-__device__ __forceinline__ const double* cm_row(const Rows& R, int64_t s, int64_t nx, int64_t rowlen, int periodic,
-                                                int& ghost_side) {
-  ghost_side = 0;
+// (boundary.py:119-130).
+__device__ __forceinline__ const double* cm_row(const Rows& R, int64_t s, int64_t nx, int64_t rowlen, int periodic) {
   if (s >= R.row0 && s < R.row0 + R.nrows) return R.base + (s - R.row0) * rowlen;
   if (s == R.row0 - 1 && R.lo) return R.lo;
   if (s == R.row0 + R.nrows && R.hi) return R.hi;
@@ -109,54 +133,50 @@ __device__ __forceinline__ const double* cm_row(const Rows& R, int64_t s, int64_
     while (s >= nx) s -= nx;
     return R.base + (s - R.row0) * rowlen;
   }
-  if (s < 0) {
-    ghost_side = 1;
-    return R.base + (0 - R.row0) * rowlen;
-  }
-  ghost_side = 2;
-  return R.base + (nx - 1 - R.row0) * rowlen;
+  return R.base + ((s < 0 ? 0 : nx - 1) - R.row0) * rowlen;  // wall: mirror node, reflected later
 }
 
-__device__ __forceinline__ int64_t cm_col(int64_t c, int64_t ny, int periodic, int& ghost_side) {
-  ghost_side = 0;
-  if (c >= 0 && c < ny) return c;
-  if (periodic) {
-    while (c < 0) c += ny;
-    while (c >= ny) c -= ny;
-    return c;
-  }
-  ghost_side = c < 0 ? 1 : 2;
-  return c < 0 ? 0 : ny - 1;
-}
+// Tile geometry: target rows [tr0, tr0 + nvr) x columns [j0, j0 + nvc);
+// source nodes s_first.., c_first.. (global indices).
+struct CMTile {
+  int64_t tr0, j0, s_first, c_first;
+  int nvr, nvc;
+};
 
-template <int M, int SCH>
-__global__ void __launch_bounds__(256, CMCfg<M, SCH>::MINB) cellmap_kernel(const __grid_constant__ CellMapArgs a) {
+// MODE is a profiling knob (tools/cellmap_probe.cu): 0 = the product kernel,
+// 1 = skip the staging copies (compute on whatever the ring holds),
+// 2 = skip the tensor-core work and stores (staging only).
+template <int M, int SCH, int MODE = 0>
+__global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(const __grid_constant__ CellMapArgs a) {
   using C = CMCfg<M, SCH>;
   constexpr int TR = C::TR, TJ = C::TJ, NT = C::NT, MT = C::MT, NS = C::NS, KSC = C::KSC, KC = C::KC,
-                KCP = C::KCP, NCH = C::NCH;
+                KCP = C::KCP, NCH = C::NCH, NW = C::NW;
   extern __shared__ __align__(16) double smem[];
-  int* s_icode = reinterpret_cast<int*>(smem + NS * C::SBUF);
-  int* s_ocode = s_icode + C::NK * 4;
+  int* s_ocode = reinterpret_cast<int*>(smem + C::EPI0 + C::EPIB);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::EPI0 + C::EPIB + (NT * 8 + 1) / 2);
+  uint64_t* full = bars;        // [NS] producer -> consumers: slot staged
+  uint64_t* empty = bars + NS;  // [NS] consumers -> producer: slot consumed
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int i = tid; i < C::NK * 4; i += blockDim.x) s_icode[i] = a.icode[i];
+
   for (int i = tid; i < NT * 8; i += blockDim.x) s_ocode[i] = a.ocode[i];
+  if (tid == 0) {
+    for (int b = 0; b < NS; ++b) {
+      mbar_init(&full[b], 2 * 32 * C::NPW);  // each producer lane: one plain arrive + one cp.async arrive
+      mbar_init(&empty[b], NW);  // one arrive per consumer warp
+    }
+  }
+  __syncthreads();
 
-  const int64_t tcols = (a.nty + TJ - 1) / TJ;
-  const int64_t ntiles = tcols * ((a.ntrows + TR - 1) / TR);
-  const int64_t my_tiles = ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int64_t nstages = my_tiles * NCH;
-  const bool walls = !a.periodic;
+  const int tcols = (int)((a.nty + TJ - 1) / TJ);
+  const int ntiles = tcols * (int)((a.ntrows + TR - 1) / TR);
+  const int my_tiles = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int nstages = my_tiles * NCH;
 
-  struct TileGeo {
-    int64_t tr0, j0, s_first, c_first;
-    int nvr, nvc;
-  };
-  auto geo = [&](int64_t g) {
-    TileGeo t;
-    const int64_t tile = blockIdx.x + (g / NCH) * (int64_t)gridDim.x;
-    const int64_t ti = tile / tcols;
-    t.tr0 = ti * TR;
-    t.j0 = (tile - ti * tcols) * TJ;
+  auto tile_geo = [&](int tile) {
+    CMTile t;
+    const int ti = tile / tcols;
+    t.tr0 = (int64_t)ti * TR;
+    t.j0 = (int64_t)(tile - ti * tcols) * TJ;
     const int64_t vr = a.ntrows - t.tr0, vc = a.nty - t.j0;
     t.nvr = vr < TR ? (int)vr : TR;
     t.nvc = vc < TJ ? (int)vc : TJ;
@@ -165,119 +185,161 @@ __global__ void __launch_bounds__(256, CMCfg<M, SCH>::MINB) cellmap_kernel(const
     return t;
   };
 
-  // Stage g = (tile, chunk): source entries [16 ch, 16 ch + 16) of the tile's
-  // (TR+1) x (TJ+1) nodes, and k-steps [4 ch, 4 ch + 4) of W.
-  auto issue = [&](int64_t g) {
-    const TileGeo t = geo(g);
-    const int ch = (int)(g % NCH);
-    double* cb = smem + (g % NS) * C::SBUF;
+  if (warp >= NW) {
+    // ------------------------------------------------------------ producers
+    // producer lane pl -> entry e = pl % KC of the chunk, node columns q = pl / KC + QL k.
+    constexpr int NPL = 32 * C::NPW;
+    constexpr int QL = NPL / KC;
+    constexpr int NQ = (TJ + QL) / QL;  // node columns per lane (ceil((TJ+1)/QL))
+    const int pl = tid - 32 * NW;
+    const int e = pl % KC, q0 = pl / KC;
+    int tile = blockIdx.x, ch = 0;
+    CMTile t = tile_geo(tile);
+    for (int g = 0; g < nstages; ++g) {
+      const int b = g % NS;
+      if (g >= NS) mbar_wait(&empty[b], ((g / NS) - 1) & 1);
+      double* cb = smem + b * C::SBUF;
+      const int slot = ch * KC + e;  // input slot: field 0 in [0, K0), field 1 in [K0, 4 NK)
+      const bool f1 = slot >= C::K0;
+      const int eo = f1 ? slot - C::K0 : slot;
+      const bool pad = eo >= (f1 ? C::P1 : C::P0);
+      const bool edge = t.s_first < 0 || t.s_first + t.nvr >= a.nx || t.c_first < 0 || t.c_first + t.nvc >= a.ny;
+      const bool manual = !a.periodic && edge;  // wall ghosts: load, reflect, store
+      double* dst = cb + q0 * KCP + e;
+      if (pad) {
 #pragma unroll 1
-    for (int idx = tid; idx < C::NODES * KC; idx += blockDim.x) {
-      const int node = idx / KC, e = idx - (idx / KC) * KC;
-      const int r = node / (TJ + 1), q = node - (node / (TJ + 1)) * (TJ + 1);
-      const int ein = ch * KC + e;
-      double* dst = cb + node * KCP + e;
-      if (ein >= C::DIN || r > t.nvr || q > t.nvc) {
-        *dst = 0.0;
-        continue;
+        for (int r = 0; r <= TR; ++r)
+#pragma unroll
+          for (int k = 0; k < NQ; ++k)
+            if (q0 + k * QL <= TJ) dst[(r * (TJ + 1) + k * QL) * KCP] = 0.0;
+      } else if (MODE != 1) {
+        const int pf = f1 ? C::P1 : C::P0;
+        const int64_t rowlen = a.ny * pf;
+        int col[NQ];  // offset of this lane's entry in each staged column (fits 32 bits: ny * P < 2^31)
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) {
+          int64_t c = t.c_first + q0 + k * QL;
+          if (c < 0) c = a.periodic ? c + a.ny : 0;
+          if (c >= a.ny) c = a.periodic ? c - a.ny : a.ny - 1;
+          col[k] = (int)c * pf + eo;
+        }
+#pragma unroll 1
+        for (int r = 0; r <= t.nvr; ++r) {
+          const double* row = f1 ? cm_row(a.f1, t.s_first + r, a.nx, rowlen, a.periodic)
+                                 : cm_row(a.f0, t.s_first + r, a.nx, rowlen, a.periodic);
+#pragma unroll
+          for (int k = 0; k < NQ; ++k)
+            if (q0 + k * QL <= t.nvc) cm_cp_async8(dst + (r * (TJ + 1) + k * QL) * KCP, row + col[k]);
+        }
+        if (manual) {
+          // wall ghosts: wait for this lane's copies, then reflect them in place
+          // (boundary.py:56-98; field 1 reflects around zero, dissipative.py:229)
+          asm volatile("cp.async.wait_all;\n" ::: "memory");
+          const int w = f1 ? C::W1 : C::W0;
+#pragma unroll 1
+          for (int r = 0; r <= t.nvr; ++r) {
+            const int64_t s = t.s_first + r;
+            const int xk = s < 0 ? a.kxl : (s >= a.nx ? a.kxh : 0);
+            const double gx = f1 ? 0.0 : (s < 0 ? a.gxl : a.gxh);
+#pragma unroll
+            for (int k = 0; k < NQ; ++k) {
+              const int q = q0 + k * QL;
+              const int64_t c = t.c_first + q;
+              const int yk = c < 0 ? a.kyl : (c >= a.ny ? a.kyh : 0);
+              if (q > t.nvc || !(xk | yk)) continue;
+              const double gy = f1 ? 0.0 : (c < 0 ? a.gyl : a.gyh);
+              double* pv = dst + (r * (TJ + 1) + k * QL) * KCP;
+              *pv = ghosted(*pv, eo / w, eo % w, xk, gx, yk, gy);
+            }
+          }
+        }
       }
-      const bool f1 = ein >= C::P0;
-      const int pf = f1 ? C::P1 : C::P0;
-      int gs;
-      const double* row = f1 ? cm_row(a.f1, t.s_first + r, a.nx, a.ny * pf, a.periodic, gs)
-                             : cm_row(a.f0, t.s_first + r, a.nx, a.ny * pf, a.periodic, gs);
-      const int64_t col = cm_col(t.c_first + q, a.ny, a.periodic, gs);
-      cm_cp_async8(dst, row + col * pf + (f1 ? ein - C::P0 : ein));
-    }
-    const int nks = (C::NK - ch * KSC) < KSC ? (C::NK - ch * KSC) : KSC;
-    const double* wsrc = a.wfrag + (size_t)ch * KSC * NT * 32;
-    double* wb = cb + C::CBUF;
+      // W fragments of the chunk (contiguous, 16-byte aligned)
+      const int nks = (C::NK - ch * KSC) < KSC ? (C::NK - ch * KSC) : KSC;
+      const double* wsrc = a.wfrag + ch * KSC * NT * 32;
+      double* wb = cb + C::CBUF;
 #pragma unroll 1
-    for (int i = tid; i < nks * NT * 16; i += blockDim.x) cm_cp_async16(wb + 2 * i, wsrc + 2 * i);
-  };
-
-  // Wall ghosts: reflect the staged copies this thread issued (boundary.py:56-98;
-  // the velocity / g1 reflects around zero, dissipative.py:229).
-  auto fix_ghosts = [&](int64_t g) {
-    const TileGeo t = geo(g);
-    if (!(t.s_first < 0 || t.s_first + t.nvr >= a.nx || t.c_first < 0 || t.c_first + t.nvc >= a.ny)) return;
-    const int ch = (int)(g % NCH);
-    double* cb = smem + (g % NS) * C::SBUF;
-#pragma unroll 1
-    for (int idx = tid; idx < C::NODES * KC; idx += blockDim.x) {
-      const int node = idx / KC, e = idx - (idx / KC) * KC;
-      const int r = node / (TJ + 1), q = node - (node / (TJ + 1)) * (TJ + 1);
-      const int ein = ch * KC + e;
-      if (ein >= C::DIN || r > t.nvr || q > t.nvc) continue;
-      const int64_t s = t.s_first + r, c = t.c_first + q;
-      const int xk = s < 0 ? a.kxl : (s >= a.nx ? a.kxh : 0);
-      const int yk = c < 0 ? a.kyl : (c >= a.ny ? a.kyh : 0);
-      if (!(xk | yk)) continue;
-      const bool f1 = ein >= C::P0;
-      const int w = f1 ? C::W1 : C::W0;
-      const int eo = f1 ? ein - C::P0 : ein;
-      const double gx = f1 ? 0.0 : (s < 0 ? a.gxl : a.gxh);
-      const double gy = f1 ? 0.0 : (c < 0 ? a.gyl : a.gyh);
-      double* p = cb + node * KCP + e;
-      *p = ghosted(*p, eo / w, eo % w, xk, gx, yk, gy);
+      for (int i = pl; i < nks * NT * 16; i += NPL) cm_cp_async16(wb + 2 * i, wsrc + 2 * i);
+      mbar_arrive(&full[b]);           // orders this lane's plain shared stores
+      mbar_arrive_cp_async(&full[b]);  // fires when this lane's copies have landed
+      if (++ch == NCH) {
+        ch = 0;
+        tile += gridDim.x;
+        if (tile < ntiles) t = tile_geo(tile);
+      }
     }
-  };
+    return;
+  }
 
+  // -------------------------------------------------------------- consumers
+  // Parity bits (kx & 1, ky & 1) of this lane's input slot 4 s + (lane & 3)
+  // at every k-step s (sign flips of the x- / y-right corners).
+  unsigned long long kxbits = 0, kybits = 0;
+#pragma unroll 1
+  for (int st = 0; st < C::NK; ++st) {
+    const int code = a.icode[st * 4 + (lane & 3)];
+    kxbits |= (unsigned long long)(code & 1) << st;
+    kybits |= (unsigned long long)((code >> 1) & 1) << st;
+  }
   double acc[MT][NT][2];
 #pragma unroll
   for (int t = 0; t < MT; ++t)
 #pragma unroll
     for (int n = 0; n < NT; ++n) acc[t][n][0] = acc[t][n][1] = 0.0;
 
+  int tile = blockIdx.x, ch = 0;
+  CMTile cg = tile_geo(tile);
+  double* st = smem + C::EPI0 + warp * 8 * C::DO;
+  for (int g = 0; g < nstages; ++g) {
+    const int b = g % NS;
+    if (SCH == kCons && ch == 0) {
+      // the epilogue subtracts `previous`: pull this warp's records toward L2
+      // while the tile's DMMAs run (8 cells x O0 doubles per M-tile, contiguous)
 #pragma unroll
-  for (int g = 0; g < NS - 1; ++g) {
-    if (g < nstages) issue(g);
-    cm_commit();
-  }
-
-  for (int64_t g = 0; g < nstages; ++g) {
-    cm_wait<NS - 2>();
-    if (walls) fix_ghosts(g);
-    __syncthreads();
-    if (g + NS - 1 < nstages) issue(g + NS - 1);
-    cm_commit();
-
-    const int ch = (int)(g % NCH);
-    const double* cb = smem + (g % NS) * C::SBUF;
+      for (int t = 0; t < MT; ++t) {
+        const int mt = warp * MT + t;
+        const int trl = mt / (TJ / 8), jl0 = (mt % (TJ / 8)) * 8;
+        if (trl < cg.nvr && jl0 < cg.nvc && lane * 16 < 8 * C::O0) {
+          const double* p = a.prev + ((cg.tr0 + trl) * a.nty + cg.j0 + jl0) * C::O0 + lane * 16;
+          asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+        }
+      }
+    }
+    mbar_wait(&full[b], (g / NS) & 1);
+    const double* cb = smem + b * C::SBUF;
     const double* wb = cb + C::CBUF;
     const int nks = (C::NK - ch * KSC) < KSC ? (C::NK - ch * KSC) : KSC;
     auto kstep = [&](const int ks) {
-      {
-        const int code = s_icode[(ch * KSC + ks) * 4 + (lane & 3)];
-        const unsigned long long mx = (unsigned long long)(code & 1) << 63;
-        const unsigned long long my = (unsigned long long)((code >> 1) & 1) << 63;
-        double A[MT][4];
+      const int step = ch * KSC + ks;
+      const unsigned long long mx = ((kxbits >> step) & 1ull) << 63;
+      const unsigned long long my = ((kybits >> step) & 1ull) << 63;
+      double A[MT][4];
 #pragma unroll
-        for (int t = 0; t < MT; ++t) {
-          const int mt = warp * MT + t;
-          const int trl = mt / (TJ / 8), tc = (mt % (TJ / 8)) * 8;
-          const double* p = cb + (trl * (TJ + 1) + tc + (lane >> 2)) * KCP + ks * 4 + (lane & 3);
-          const double c00 = p[0];
-          const double c01 = flip_sign(p[KCP], my);
-          const double c10 = flip_sign(p[(TJ + 1) * KCP], mx);
-          const double c11 = flip_sign(p[(TJ + 2) * KCP], mx ^ my);
-          const double ap = c00 + c10, am = c00 - c10, bp = c01 + c11, bm = c01 - c11;
-          A[t][0] = ap + bp;  // class (0,0)
-          A[t][1] = ap - bp;  // class (0,1)
-          A[t][2] = am + bm;  // class (1,0)
-          A[t][3] = am - bm;  // class (1,1)
-        }
-        const double* wk = wb + ks * NT * 32 + lane;
+      for (int t = 0; t < MT; ++t) {
+        const int mt = warp * MT + t;
+        const int trl = mt / (TJ / 8), tc = (mt % (TJ / 8)) * 8;
+        const double* p = cb + (trl * (TJ + 1) + tc + (lane >> 2)) * KCP + ks * 4 + (lane & 3);
+        const double c00 = p[0];
+        const double c01 = flip_sign(p[KCP], my);
+        const double c10 = flip_sign(p[(TJ + 1) * KCP], mx);
+        const double c11 = flip_sign(p[(TJ + 2) * KCP], mx ^ my);
+        const double ap = c00 + c10, am = c00 - c10, bp = c01 + c11, bm = c01 - c11;
+        A[t][0] = ap + bp;  // class (0,0)
+        A[t][1] = ap - bp;  // class (0,1)
+        A[t][2] = am + bm;  // class (1,0)
+        A[t][3] = am - bm;  // class (1,1)
+      }
+      const double* wk = wb + ks * NT * 32 + lane;
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const int c = nt < C::B1 ? 0 : (nt < C::B2 ? 1 : (nt < C::B3 ? 2 : 3));  // parity class of tile nt
-          const double b = wk[nt * 32];
+      for (int nt = 0; nt < NT; ++nt) {
+        const int c = nt < C::B1 ? 0 : (nt < C::B2 ? 1 : (nt < C::B3 ? 2 : 3));  // parity class of tile nt
+        const double bf = wk[nt * 32];
 #pragma unroll
-          for (int t = 0; t < MT; ++t) dmma(acc[t][nt], A[t][c], b);
-        }
+        for (int t = 0; t < MT; ++t) dmma(acc[t][nt], A[t][c], bf);
       }
     };
-    if constexpr (C::UNROLL_KS) {
+    if constexpr (MODE == 2) {
+    } else if constexpr (C::UNROLL_KS) {
 #pragma unroll
       for (int ks = 0; ks < KSC; ++ks)
         if (ks < nks) kstep(ks);
@@ -285,38 +347,60 @@ __global__ void __launch_bounds__(256, CMCfg<M, SCH>::MINB) cellmap_kernel(const
 #pragma unroll 1
       for (int ks = 0; ks < nks; ++ks) kstep(ks);
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[b]);  // slot b may be refilled
 
-    if (ch == NCH - 1) {  // epilogue: this tile's outputs straight to global
-      const TileGeo tg = geo(g);
+    if (ch == NCH - 1) {
+      // Epilogue, one M-tile at a time through this warp's staging slab: the
+      // fragments land in record order (ocode = position in the node's output
+      // record, -1 = padding), then the 8 cells' records — contiguous in the
+      // output fields — are written with consecutive lanes on consecutive
+      // doubles.
 #pragma unroll
       for (int t = 0; t < MT; ++t) {
         const int mt = warp * MT + t;
-        const int trl = mt / (TJ / 8), jl = (mt % (TJ / 8)) * 8 + (lane >> 2);
-        if (trl < tg.nvr && jl < tg.nvc) {
-          const int64_t cell = (tg.tr0 + trl) * a.nty + tg.j0 + jl;
+        const int trl = mt / (TJ / 8), jl0 = (mt % (TJ / 8)) * 8;
+        const int nv = trl < cg.nvr ? (cg.nvc - jl0 < 8 ? cg.nvc - jl0 : 8) : 0;
 #pragma unroll
-          for (int n = 0; n < NT; ++n)
+        for (int n = 0; n < NT; ++n)
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
-              const int code = s_ocode[n * 8 + (lane & 3) * 2 + i];
-              if (code < 0) continue;
-              const int o = code & 0xffff;
-              if ((code >> 16) == 0) {
-                const int64_t idx = cell * C::O0 + o;
-                double v = acc[t][n][i];
-                if (SCH == kCons) v -= a.prev[idx];
-                a.out0[idx] = v;
-              } else {
-                a.out1[cell * C::O1 + o] = acc[t][n][i];
-              }
+          for (int i = 0; i < 2; ++i) {
+            const int pos = s_ocode[n * 8 + (lane & 3) * 2 + i];
+            if (pos >= 0) st[(lane >> 2) * C::DO + pos] = acc[t][n][i];
+            acc[t][n][i] = 0.0;
+          }
+        __syncwarp();
+        if (MODE != 2 && nv > 0) {
+          const int64_t cell0 = (cg.tr0 + trl) * a.nty + cg.j0 + jl0;
+          double* o0 = a.out0 + cell0 * C::O0;
+          const double* p0 = a.prev + cell0 * C::O0;
+#pragma unroll
+          for (int k = 0; k < (8 * C::O0 + 31) / 32; ++k) {
+            const int q = lane + 32 * k;
+            if (q < nv * C::O0) {
+              double v = st[(q / C::O0) * C::DO + q % C::O0];
+              if (SCH == kCons) v -= p0[q];
+              o0[q] = v;
             }
-        }
+          }
+          if (C::O1 > 0) {
+            double* o1 = a.out1 + cell0 * C::O1;
 #pragma unroll
-        for (int n = 0; n < NT; ++n) acc[t][n][0] = acc[t][n][1] = 0.0;
+            for (int k = 0; k < (8 * C::O1 + 31) / 32; ++k) {
+              const int q = lane + 32 * k;
+              if (q < nv * C::O1) o1[q] = st[(q / C::O1) * C::DO + C::O0 + q % C::O1];
+            }
+          }
+        }
+        __syncwarp();
       }
+      ch = 0;
+      tile += gridDim.x;
+      if (tile < ntiles) cg = tile_geo(tile);
+    } else {
+      ++ch;
     }
   }
-  cm_wait<0>();
 }
 
 }  // namespace hw

@@ -13,19 +13,20 @@ template <int M, int SCH>
 cudaError_t launch_cellmap(const CellMapArgs& a, cudaStream_t st) {
   using C = CMCfg<M, SCH>;
   static_assert(C::SMEM <= 227 * 1024, "stage ring exceeds the 227 KB shared-memory limit");
+  static_assert(C::NK <= 64, "per-lane parity bit masks hold at most 64 k-steps");
   auto kern = cellmap_kernel<M, SCH>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
   int dev = 0, nsm = 0, per_sm = 0;
   if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
   if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * C::NW, C::SMEM)) != cudaSuccess)
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::NTHREADS, C::SMEM)) != cudaSuccess)
     return e;
   const int64_t ntiles = ((a.nty + C::TJ - 1) / C::TJ) * ((a.ntrows + C::TR - 1) / C::TR);
   int64_t nblk = (int64_t)nsm * (per_sm > 0 ? per_sm : 1);
   if (nblk > ntiles) nblk = ntiles;
   if (nblk <= 0) return cudaSuccess;
-  kern<<<(unsigned)nblk, 32 * C::NW, C::SMEM, st>>>(a);
+  kern<<<(unsigned)nblk, C::NTHREADS, C::SMEM, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -37,7 +37,12 @@ constexpr int cm_class_of_tile(int sch, int m, int nt) {
   return nt < cm_ntbase(sch, m, 1) ? 0 : (nt < cm_ntbase(sch, m, 2) ? 1 : (nt < cm_ntbase(sch, m, 3) ? 2 : 3));
 }
 
-// 4-deep input steps (DMMA K = 4)
-constexpr int cm_nk(int sch, int m) { return (cm_din(sch, m) + 3) / 4; }
+// Input slots: each field's entries padded to a multiple of 4 (a 4-deep
+// DMMA k-step never straddles the two fields): field 0 in [0, K0), field 1
+// from K0.  k-steps of 4 slots: NK.
+constexpr int cm_k0(int sch, int m) { return (cm_win(sch, m, 0) * cm_win(sch, m, 0) + 3) / 4 * 4; }
+constexpr int cm_nk(int sch, int m) {
+  return (cm_k0(sch, m) + (cm_win(sch, m, 1) * cm_win(sch, m, 1) + 3) / 4 * 4) / 4;
+}
 
 }  // namespace hw

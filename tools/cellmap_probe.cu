@@ -1,0 +1,87 @@
+// Where does the cell-map kernel's time go?  Times the product kernel against
+// variants without staging (MODE 1) and without tensor-core work (MODE 2) on
+// a periodic n x n grid of random data (values are irrelevant here).
+//   tools/cellmap_probe [n]
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../paper_1802_05246_b200/csrc/cellmap.cuh"
+
+using namespace hw;
+
+template <int M, int SCH, int MODE>
+float time_variant(const CellMapArgs& a) {
+  using C = CMCfg<M, SCH>;
+  auto k = cellmap_kernel<M, SCH, MODE>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  int nsm = 0, per = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, C::NTHREADS, C::SMEM);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(e0);
+    k<<<nsm * per, C::NTHREADS, C::SMEM>>>(a);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (r > 0 && ms < best) best = ms;
+  }
+  return best * (per > 0 ? 1.0f : -1.0f);
+}
+
+template <int M, int SCH>
+void probe(int64_t n) {
+  using C = CMCfg<M, SCH>;
+  CellMapArgs a;
+  memset(&a, 0, sizeof(a));
+  double *f0, *f1, *o0, *o1, *w;
+  int *oc, *ic;
+  cudaMalloc(&f0, n * n * C::P0 * 8);
+  cudaMalloc(&f1, n * n * (C::P1 ? C::P1 : 1) * 8);
+  cudaMalloc(&o0, n * n * C::O0 * 8);
+  cudaMalloc(&o1, n * n * (C::O1 ? C::O1 : 1) * 8);
+  cudaMalloc(&w, C::NK * C::NT * 32 * 8);
+  cudaMalloc(&oc, C::NT * 8 * 4);
+  cudaMalloc(&ic, C::NK * 4 * 4);
+  cudaMemset(f0, 0, n * n * C::P0 * 8);
+  cudaMemset(f1, 0, n * n * (C::P1 ? C::P1 : 1) * 8);
+  cudaMemset(w, 0, C::NK * C::NT * 32 * 8);
+  std::vector<int> h(C::NT * 8);
+  for (int i = 0; i < C::NT * 8; ++i) h[i] = i % C::O0;
+  cudaMemcpy(oc, h.data(), h.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemset(ic, 0, C::NK * 4 * 4);
+  a.f0 = {f0, nullptr, nullptr, 0, n};
+  a.f1 = {f1, nullptr, nullptr, 0, n};
+  a.wfrag = w;
+  a.ocode = oc;
+  a.icode = ic;
+  a.prev = o0;
+  a.out0 = o0;
+  a.out1 = o1;
+  a.nx = a.ny = n;
+  a.trow0 = 0;
+  a.ntrows = n;
+  a.nty = n;
+  a.periodic = 1;
+  const float t0 = time_variant<M, SCH, 0>(a);
+  const float t1 = time_variant<M, SCH, 1>(a);
+  const float t2 = time_variant<M, SCH, 2>(a);
+  printf("{\"m\": %d, \"scheme\": %d, \"n\": %ld, \"full_ms\": %.4f, \"no_staging_ms\": %.4f, \"staging_only_ms\": %.4f, "
+         "\"err\": \"%s\"}\n",
+         M, SCH, (long)n, t0, t1, t2, cudaGetErrorString(cudaDeviceSynchronize()));
+  cudaFree(f0); cudaFree(f1); cudaFree(o0); cudaFree(o1); cudaFree(w); cudaFree(oc); cudaFree(ic);
+}
+
+int main(int argc, char** argv) {
+  const int64_t n = argc > 1 ? atoll(argv[1]) : 1024;
+  probe<4, kDiss>(n);
+  probe<6, kDiss>(n);
+  probe<8, kDiss>(n);
+  probe<5, kCons>(n);
+  return 0;
+}
