@@ -134,11 +134,7 @@ static DevMap device_map(int scheme, int m, double dt, double hx, double hy, dou
   for (int c = 0; c < 4; ++c) {
     if (cm.ncls[c] != cm_ncls(scheme, m, c)) throw Error(HW_EINVAL, "internal: class size mismatch");
     const int base = cm_ntbase(scheme, m, c);
-    const int o0 = cm.w_out[0] * cm.w_out[0];
-    for (int o = 0; o < cm.ncls[c]; ++o) {  // position in the [field 0 | field 1] output record
-      const int code = cm.code[c][o];
-      oc[(size_t)(base + o / 8) * 8 + o % 8] = (code >> 16 ? o0 : 0) + (code & 0xffff);
-    }
+    for (int o = 0; o < cm.ncls[c]; ++o) oc[(size_t)(base + o / 8) * 8 + o % 8] = cm.code[c][o];
     for (int ks = 0; ks < nk; ++ks)
       for (int j = 0; j < cm_ntc(scheme, m, c); ++j)
         for (int lane = 0; lane < 32; ++lane) {

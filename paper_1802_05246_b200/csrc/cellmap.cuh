@@ -31,7 +31,7 @@ namespace hw {
 struct CellMapArgs {
   Rows f0, f1;                 // source fields (f1 unused when the scheme has one input)
   const double* wfrag;         // [NK][NT][32] B fragments
-  const int* ocode;            // [NT][8] position in the cell's [field 0 | field 1] output record, -1 = padding
+  const int* ocode;            // [NT][8] output field << 16 | offset in its record, -1 = padding
   const int* icode;            // [NK*4] (kx & 1) | (ky & 1) << 1 of each input slot
   const double* prev;          // kCons: previous level (may alias out0)
   double* out0;
@@ -70,7 +70,8 @@ struct CMCfg {
   static constexpr int SBUF = CBUF + WBUF;         // doubles per ring slot
   static constexpr int DO = O0 + O1;               // output record per cell
   static constexpr int EPIB = NW * 8 * DO;         // per-warp epilogue staging (doubles)
-  static constexpr int TAIL = EPIB * 8 + NT * 8 * 4 + 64;
+  static constexpr int PREVB = SCH == kCons ? NW * MT * 8 * O0 : 0;  // kCons: `previous` of the warp's cells
+  static constexpr int TAIL = (EPIB + PREVB) * 8 + NT * 8 * 4 + 64;
   static constexpr int NS = (4 * SBUF * 8 + TAIL <= 227 * 1024) ? 4 : 3;  // ring depth
   static constexpr int EPI0 = NS * SBUF;           // double offset of the staging slabs
   static constexpr int SMEM = NS * SBUF * 8 + TAIL;
@@ -109,6 +110,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+// Producer-side wait: back off between polls so a producer that runs ahead
+// of the ring does not steal issue slots from the consumer warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) {
+  unsigned ok = 0;
+  while (true) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) break;
+    __nanosleep(128);
+  }
 }
 
 // D += A B on the FP64 tensor cores (one 8x8x4 tile per warp).
@@ -152,8 +172,9 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
   constexpr int TR = C::TR, TJ = C::TJ, NT = C::NT, MT = C::MT, NS = C::NS, KSC = C::KSC, KC = C::KC,
                 KCP = C::KCP, NCH = C::NCH, NW = C::NW;
   extern __shared__ __align__(16) double smem[];
-  int* s_ocode = reinterpret_cast<int*>(smem + C::EPI0 + C::EPIB);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::EPI0 + C::EPIB + (NT * 8 + 1) / 2);
+  double* s_prev = smem + C::EPI0 + C::EPIB;
+  int* s_ocode = reinterpret_cast<int*>(smem + C::EPI0 + C::EPIB + C::PREVB);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::EPI0 + C::EPIB + C::PREVB + (NT * 8 + 1) / 2);
   uint64_t* full = bars;        // [NS] producer -> consumers: slot staged
   uint64_t* empty = bars + NS;  // [NS] consumers -> producer: slot consumed
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -197,7 +218,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
     CMTile t = tile_geo(tile);
     for (int g = 0; g < nstages; ++g) {
       const int b = g % NS;
-      if (g >= NS) mbar_wait(&empty[b], ((g / NS) - 1) & 1);
+      if (g >= NS) mbar_wait_sleep(&empty[b], ((g / NS) - 1) & 1);
       double* cb = smem + b * C::SBUF;
       const int slot = ch * KC + e;  // input slot: field 0 in [0, K0), field 1 in [K0, 4 NK)
       const bool f1 = slot >= C::K0;
@@ -212,6 +233,20 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
 #pragma unroll
           for (int k = 0; k < NQ; ++k)
             if (q0 + k * QL <= TJ) dst[(r * (TJ + 1) + k * QL) * KCP] = 0.0;
+      } else if (MODE != 1 && t.nvr == TR && t.nvc == TJ && t.s_first >= a.f0.row0 &&
+                 t.s_first + TR < a.f0.row0 + a.f0.nrows && t.c_first >= 0 && t.c_first + TJ < a.ny) {
+        // interior tile: every staged row is a dense segment of the local slab
+        const int pf = f1 ? C::P1 : C::P0;
+        const int64_t rowlen = a.ny * pf;
+        const double* src = (f1 ? a.f1.base : a.f0.base) + (t.s_first - a.f0.row0) * rowlen + (t.c_first + q0) * pf + eo;
+        const int cstep = QL * pf;
+#pragma unroll
+        for (int r = 0; r <= TR; ++r) {
+#pragma unroll
+          for (int k = 0; k < NQ; ++k)
+            if (k < NQ - 1 || q0 + k * QL <= TJ) cm_cp_async8(dst + (r * (TJ + 1) + k * QL) * KCP, src + k * cstep);
+          src += rowlen;
+        }
       } else if (MODE != 1) {
         const int pf = f1 ? C::P1 : C::P0;
         const int64_t rowlen = a.ny * pf;
@@ -293,16 +328,17 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
   for (int g = 0; g < nstages; ++g) {
     const int b = g % NS;
     if (SCH == kCons && ch == 0) {
-      // the epilogue subtracts `previous`: pull this warp's records toward L2
-      // while the tile's DMMAs run (8 cells x O0 doubles per M-tile, contiguous)
+      // the epilogue subtracts `previous`: stage this warp's records (8 cells
+      // x O0 doubles per M-tile, contiguous) with cp.async now, so they land
+      // while the tile's DMMAs run
 #pragma unroll
       for (int t = 0; t < MT; ++t) {
         const int mt = warp * MT + t;
         const int trl = mt / (TJ / 8), jl0 = (mt % (TJ / 8)) * 8;
-        if (trl < cg.nvr && jl0 < cg.nvc && lane * 16 < 8 * C::O0) {
-          const double* p = a.prev + ((cg.tr0 + trl) * a.nty + cg.j0 + jl0) * C::O0 + lane * 16;
-          asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
-        }
+        const int nv = trl < cg.nvr ? (cg.nvc - jl0 < 8 ? cg.nvc - jl0 : 8) : 0;
+        const double* p = a.prev + ((cg.tr0 + trl) * a.nty + cg.j0 + jl0) * C::O0;
+        double* d = s_prev + (warp * MT + t) * 8 * C::O0;
+        for (int q = lane; q < nv * C::O0; q += 32) cm_cp_async8(d + q, p + q);
       }
     }
     mbar_wait(&full[b], (g / NS) & 1);
@@ -351,11 +387,12 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
     if (lane == 0) mbar_arrive(&empty[b]);  // slot b may be refilled
 
     if (ch == NCH - 1) {
-      // Epilogue, one M-tile at a time through this warp's staging slab: the
-      // fragments land in record order (ocode = position in the node's output
-      // record, -1 = padding), then the 8 cells' records — contiguous in the
-      // output fields — are written with consecutive lanes on consecutive
-      // doubles.
+      // Epilogue, one M-tile at a time through this warp's staging slab, laid
+      // out exactly like the outputs: [8 records of field 0][8 records of
+      // field 1].  The fragments land at their record positions (ocode =
+      // field << 16 | offset, -1 = padding); the 8 cells' records, contiguous
+      // in each output field, are then written by consecutive lanes.
+      const int base0 = (lane >> 2) * C::O0, base1 = 8 * C::O0 + (lane >> 2) * C::O1;
 #pragma unroll
       for (int t = 0; t < MT; ++t) {
         const int mt = warp * MT + t;
@@ -365,20 +402,21 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
         for (int n = 0; n < NT; ++n)
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
-            const int pos = s_ocode[n * 8 + (lane & 3) * 2 + i];
-            if (pos >= 0) st[(lane >> 2) * C::DO + pos] = acc[t][n][i];
+            const int code = s_ocode[n * 8 + (lane & 3) * 2 + i];
+            if (code >= 0) st[(code >> 16 ? base1 : base0) + (code & 0xffff)] = acc[t][n][i];
             acc[t][n][i] = 0.0;
           }
         __syncwarp();
+        if (SCH == kCons) asm volatile("cp.async.wait_all;\n" ::: "memory");
         if (MODE != 2 && nv > 0) {
           const int64_t cell0 = (cg.tr0 + trl) * a.nty + cg.j0 + jl0;
           double* o0 = a.out0 + cell0 * C::O0;
-          const double* p0 = a.prev + cell0 * C::O0;
+          const double* p0 = s_prev + (warp * MT + t) * 8 * C::O0;
 #pragma unroll
           for (int k = 0; k < (8 * C::O0 + 31) / 32; ++k) {
             const int q = lane + 32 * k;
             if (q < nv * C::O0) {
-              double v = st[(q / C::O0) * C::DO + q % C::O0];
+              double v = st[q];
               if (SCH == kCons) v -= p0[q];
               o0[q] = v;
             }
@@ -388,7 +426,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
 #pragma unroll
             for (int k = 0; k < (8 * C::O1 + 31) / 32; ++k) {
               const int q = lane + 32 * k;
-              if (q < nv * C::O1) o1[q] = st[(q / C::O1) * C::DO + C::O0 + q % C::O1];
+              if (q < nv * C::O1) o1[q] = st[8 * C::O0 + q];
             }
           }
         }
