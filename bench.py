@@ -11,13 +11,16 @@ coefficient advanced one half step: (m+1)^2 + m^2 = 41 per node.
 
 N > 1 (torchrun, one rank per GPU): weak scaling, each rank owns a
 1024 x 1024 slab of a (1024 N) x 1024 periodic grid and exchanges one node
-row per half step with its ring neighbour over NCCL.
+row per half step with its ring neighbour (torch.distributed P2P over NCCL).
+
+Extra keys beside the contract's: "c3" (conservative m=5, 2048^2,
+Dirichlet/Neumann walls — BASELINE configs[2]) and "sweep" (dissipative
+m=4..8 at ~2^30 DOF per level — configs[3]), both device resident.
 """
 
 from __future__ import annotations
 
 import argparse
-import ctypes as C
 import json
 import math
 import os
@@ -32,24 +35,53 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Hermite DOF-updates/s (FP64) 2D m=4..8 at 1/2/4/8 B200; % of FP64/HBM roofline"
 UNIT = "GDOF-updates/s"
+SWEEP_N = {2: 9088, 3: 6554, 4: 5118, 5: 4196, 6: 3554, 7: 3083, 8: 2721}  # ~2^30 DOF
+
+
+# --------------------------------------------------------------- roofline model
+
+def _I(mux, muy, rx, ry):
+    return 2 * (muy + 1) * (2 * (mux + 1) + rx * 2 * (mux + 1)) + rx * (2 * (muy + 1) + ry * 2 * (muy + 1))
+
+
+def _N(t, k):
+    return 0 if k > t else (t - k) // 2 + 1
 
 
 def f_alg_diss(m: int) -> int:
-    """Canonical symmetric-split live flop count per target cell."""
-    def I(mux, muy, rx, ry):
-        return 2 * (muy + 1) * (2 * (mux + 1) + rx * 2 * (mux + 1)) + rx * (2 * (muy + 1) + ry * 2 * (muy + 1))
-
-    def N(t, k):
-        return 0 if k > t else (t - k) // 2 + 1
-
-    taps = sum(N(2 * m - 1, k) * N(2 * m - 1, l) for k in range(m + 1) for l in range(m + 1))
-    taps += sum(N(2 * m - 1, k) * N(2 * m - 1, l) for k in range(m) for l in range(m))
-    return (I(m, m, m + 1, m + 1) + I(m, m - 1, 2 * m, 2 * m) + I(m - 1, m, 2 * m, 2 * m)
-            + I(m - 1, m - 1, 2 * m, 2 * m) + 3 * (2 * m) ** 2 + 4 * taps + (m + 1) ** 2)
+    """Canonical symmetric-split live flop count per target cell, dissipative."""
+    taps = sum(_N(2 * m - 1, k) * _N(2 * m - 1, l) for k in range(m + 1) for l in range(m + 1))
+    taps += sum(_N(2 * m - 1, k) * _N(2 * m - 1, l) for k in range(m) for l in range(m))
+    return (_I(m, m, m + 1, m + 1) + _I(m, m - 1, 2 * m, 2 * m) + _I(m - 1, m, 2 * m, 2 * m)
+            + _I(m - 1, m - 1, 2 * m, 2 * m) + 3 * (2 * m) ** 2 + 4 * taps + (m + 1) ** 2)
 
 
-def dof_per_node(m: int) -> int:
-    return (m + 1) ** 2 + m * m
+def f_alg_cons(m: int) -> int:
+    """Canonical flop count per target cell, conservative."""
+    taps = sum(_N(2 * m + 1, k) * _N(2 * m + 1, l) for k in range(m + 1) for l in range(m + 1))
+    return _I(m, m, 2 * m + 2, 2 * m + 2) + 2 * taps + 2 * (m + 1) ** 2
+
+
+def dof_per_node(m: int, scheme: str = "diss") -> int:
+    return (m + 1) ** 2 + m * m if scheme == "diss" else (m + 1) ** 2
+
+
+def cellmap_flops(m: int, scheme: str = "diss"):
+    """(dense, issued) FP64 flops per target cell of the cell-map kernel:
+    dense = 2 D_out D_in (the class maps, unpadded); issued = the DMMA tiles
+    actually executed (outputs padded to 8 per class, inputs to 4 per field)."""
+    w0, w1 = m + 1, (m if scheme == "diss" else 0)
+    din, dout = w0 * w0 + w1 * w1, w0 * w0 + w1 * w1
+    if scheme == "cons":
+        din = dout = w0 * w0
+
+    def cnt(w, p):
+        return (w - 1 - p) // 2 + 1 if w > p else 0
+
+    ncls = [cnt(w0, c >> 1) * cnt(w0, c & 1) + cnt(w1, c >> 1) * cnt(w1, c & 1) for c in range(4)]
+    kslots = 4 * ((w0 * w0 + 3) // 4) + 4 * ((w1 * w1 + 3) // 4)
+    nslots = sum(8 * ((n + 7) // 8) for n in ncls)
+    return 2 * din * dout, 2 * kslots * nslots
 
 
 def load_json(path):
@@ -58,6 +90,14 @@ def load_json(path):
             return json.load(f)
     except Exception:
         return None
+
+
+def peaks():
+    mp = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
+    fp = load_json(os.path.join(ROOT, "profiles", "fp64_peak.json")) or {}
+    dmma = fp.get("dmma_tflops")
+    return {"hbm_gbs": mp.get("hbm_gbs", 6650.0), "hbm_src": "measured" if "hbm_gbs" in mp else "fallback",
+            "dmma_tflops": dmma or 37.2, "dmma_src": "measured (tools/fp64_peak.cu)" if dmma else "datasheet-class"}
 
 
 class ClockSampler:
@@ -124,7 +164,7 @@ def cpu_sample(m: int, n: int, rows: int, lam: float = 0.9):
     step for step the reference's own numpy ops; pinned bitwise against the
     reference's golden vectors) on a `rows` x n window of the n x n workload.
     Returns (seconds, DOF-updates)."""
-    import numpy as np
+    import numpy as np  # noqa: F401
 
     from oracle import hermite_oracle as O
 
@@ -188,6 +228,7 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c3", action="store_true")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -202,7 +243,6 @@ def main():
     import torch.distributed as dist
 
     import paper_1802_05246_b200 as hb
-    from paper_1802_05246_b200 import _lib as L
     from paper_1802_05246_b200.slab import SlabRing
 
     torch.cuda.set_device(local)
@@ -212,9 +252,7 @@ def main():
     lam = 0.9
     nx_glob = n * world
     grid = hb.Grid2D(0.0, float(world), 0.0, 1.0, nx_glob, n, True)  # h = 1/n on both axes
-    h = grid.hx
     cfg = hb.SchemeConfig(m=m, lam=lam)
-    dt = cfg.dt(h)
     t0 = 0.1
     w = 2.0 * math.pi
     om = w * math.sqrt(2.0)
@@ -268,40 +306,40 @@ def main():
     dofs = cells_total * dof_per_node(m) * args.steps
     value = dofs / sec / 1e9
 
-    # roofline of the dominant kernel (diss2d_kernel<m>): FP64-pipe bound for m >= 3
+    # roofline of the dominant kernel (cellmap_kernel<m, diss>): FP64 tensor
+    # pipe (DMMA).  achieved = SURVEY §8d's canonical flops per cell x cells /
+    # kernel time; "dense"/"issued" are what this kernel's cell maps execute.
+    pk = peaks()
     cells_rank = ring.nrows * n
-    flops = f_alg_diss(m) * cells_rank
-    achieved_tf = flops / (kern_ms / 1e3) / 1e12
-    peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
-    fp64 = load_json(os.path.join(ROOT, "profiles", "fp64_peak.json")) or {}
-    p64 = fp64.get("dfma_tflops")
-    p64_src = "measured DFMA microbenchmark (profiles/fp64_peak.json)" if p64 else \
-        "datasheet-class 148 SM x 64 FMA x 2 x 1.965 GHz (no measurement found)"
-    p64 = p64 or 37.2
-    hbm = peaks.get("hbm_gbs", 6562.6)
+    ksec = kern_ms / 1e3
+    achieved = f_alg_diss(m) * cells_rank / ksec / 1e12
+    dense, issued = cellmap_flops(m)
     bytes_alg = 16 * cells_rank * dof_per_node(m)
-    achieved_gbs = bytes_alg / (kern_ms / 1e3) / 1e9
-    ncu = load_json(os.path.join(ROOT, "profiles", "ncu_summary_r01.json")) or {}
-    traffic = None
-    key = f"diss2d_m{m}_n{n}"
-    if key in ncu.get("dram_bytes_per_launch", {}):
-        traffic = ncu["dram_bytes_per_launch"][key]
-
+    ncu = load_json(os.path.join(ROOT, "profiles", "ncu_summary.json")) or {}
+    traffic = (ncu.get("launches", {}).get(f"diss_m{m}_n{n}") or {}).get("dram_bytes")
+    roofline = {
+        "bound": "tensor", "achieved": achieved, "peak": pk["dmma_tflops"], "unit": "TFLOP/s",
+        "frac": achieved / pk["dmma_tflops"], "traffic": traffic,
+        "peak_source": pk["dmma_src"] + ": FP64 DMMA (mma.sync m8n8k4 f64) — the tensor path this kernel runs on",
+        "flops_per_cell_alg": f_alg_diss(m), "kernel_ms": kern_ms,
+        "dense_map_tflops": dense * cells_rank / ksec / 1e12,
+        "issued_dmma_tflops": issued * cells_rank / ksec / 1e12,
+        "issued_frac": issued * cells_rank / ksec / 1e12 / pk["dmma_tflops"],
+        "hbm": {"achieved": bytes_alg / ksec / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": bytes_alg / ksec / 1e9 / pk["hbm_gbs"], "bytes_per_dof": 16, "peak_source": pk["hbm_src"]},
+    }
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic standing wave (no dataset)",
         "config": {"workload": f"2D periodic dissipative Hermite m={m}, {n}x{n} nodes per GPU, lambda 0.9 (C2)",
-                   "m": m, "nodes_per_gpu": [n, n], "global_nodes": [nx_glob, n], "dof_per_node": dof_per_node(m),
-                   "l2": "inputs larger than L2 (u+v = %.0f MB per parity, L2 126 MB)" % (
+                   "m": m, "nodes_per_gpu": [ring.nrows, n], "global_nodes": [nx_glob, n],
+                   "dof_per_node": dof_per_node(m),
+                   "l2": "inputs larger than L2 (u+v = %.0f MB per parity, L2 126 MB); no flush" % (
                        cells_rank * dof_per_node(m) * 8 / 1e6),
                    "parallelism": f"slab{world}" if world > 1 else "single"},
-        "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": p64, "unit": "TFLOP/s",
-                     "frac": achieved_tf / p64, "traffic": traffic, "peak_source": p64_src,
-                     "flops_per_cell": f_alg_diss(m), "kernel_ms": kern_ms,
-                     "hbm": {"achieved": achieved_gbs, "peak": hbm, "unit": "GB/s", "frac": achieved_gbs / hbm,
-                             "bytes_per_dof": 16}},
-        "gpu_launches": args.steps,
+        "roofline": roofline,
+        "gpu_launches": args.steps * (1 if world == 1 else 2),
         "clocks": clk.summary(),
     }
 
@@ -312,8 +350,10 @@ def main():
         result["cpu_baseline"] = {"value": d_cpu / t_cpu / 1e9, "unit": UNIT, "cores": 1, "kind": "port",
                                   "sample": f"one half step on a {args.cpu_rows}x{n} window of the {n}x{n} "
                                             f"grid (numpy restatement of hermwave.half_step_2d)"}
+    if rank == 0 and world == 1 and not args.no_c3:
+        result["c3"] = c3_bench(hb, torch, pk)
     if rank == 0 and world == 1 and not args.no_sweep:
-        result["sweep"] = sweep(hb, torch, p64)
+        result["sweep"] = sweep(hb, torch, pk)
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
@@ -322,7 +362,8 @@ def main():
 
 def e2e_bench(hb, torch, np, m, n, cfg, steps):
     """Same metric through the public drop-in API with host buffers:
-    hb.half_step_2d(FieldPair of numpy arrays) per step (H2D + kernel + D2H)."""
+    hb.half_step_2d(FieldPair of numpy arrays) per step — H2D of the step's
+    inputs from pinned memory, the kernel, D2H of the new state."""
     grid = hb.Grid2D(0.0, 1.0, 0.0, 1.0, n, n, True)
     w = 2.0 * math.pi
     u = hb.standing_wave_on_grid(grid, hb.PRIMAL, 0.1, m, m, w, w, w * math.sqrt(2.0), tder=0)
@@ -333,7 +374,8 @@ def e2e_bench(hb, torch, np, m, n, cfg, steps):
     hv.copy_(v)
     pair = hb.FieldPair(hb.Field2D(grid, hb.PRIMAL, 0.1, hu.numpy()), hb.Field2D(grid, hb.PRIMAL, 0.1, hv.numpy()))
     bc = hb.BoundarySpec2D()
-    hb.half_step_2d(pair, cfg, bc)  # warm-up
+    p = hb.half_step_2d(pair, cfg, bc)  # warm-up (also fills the pinned caching allocator)
+    p = hb.half_step_2d(p, cfg, bc)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     p = pair
@@ -343,45 +385,88 @@ def e2e_bench(hb, torch, np, m, n, cfg, steps):
     sec = time.perf_counter() - t0
     nbytes = (hu.numel() + hv.numel()) * 8
     return {"value": n * n * dof_per_node(m) * steps / sec / 1e9, "unit": UNIT, "h2d_bytes_per_step": nbytes,
-            "d2h_bytes_per_step": nbytes, "api": "paper_1802_05246_b200.half_step_2d(numpy FieldPair)",
-            "steps": steps}
+            "d2h_bytes_per_step": nbytes, "api": "paper_1802_05246_b200.half_step_2d(numpy FieldPair, pinned)",
+            "steps": steps, "timer": "host wall clock around the API calls"}
 
 
-def sweep(hb, torch, p64):
+def _time_steps(torch, fn, k):
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for i in range(k):
+        fn(i)
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / 1e3 / k
+
+
+def c3_bench(hb, torch, pk):
+    """Config C3: conservative m=5 on 2048^2 with Dirichlet x / Neumann y walls
+    (device resident, in place over `previous`)."""
+    from paper_1802_05246_b200.stepping import cons2d_into
+
+    m, n = 5, 2048
+    grid = hb.Grid2D(0.0, 1.0, 0.0, 1.0, n, n, False)
+    cfg = hb.SchemeConfig(m=m, lam=0.9)
+    bc = hb.BoundarySpec2D(hb.BoundarySpec("dirichlet0", "dirichlet0"), hb.BoundarySpec("neumann0", "neumann0"))
+    pi = math.pi
+    om = pi * math.sqrt(2.0)
+    dt = cfg.dt(grid.hx)
+    # u = sin(pi x) cos(pi y) cos(sqrt2 pi t) = sin(pi x) sin(pi y + pi/2) ...
+    a = hb.standing_wave_on_grid(grid, hb.PRIMAL, 0.0, m, m, pi, pi, om, py=0.5 * pi)
+    b = hb.standing_wave_on_grid(grid, hb.DUAL, -0.5 * dt, m, m, pi, pi, om, py=0.5 * pi)
+    par = [hb.PRIMAL, hb.DUAL]
+    state = {"a": a, "b": b, "pa": hb.PRIMAL}
+
+    def one(i):
+        cons2d_into(state["a"], state["b"], state["b"], grid, state["pa"], m, cfg, bc)
+        state["a"], state["b"] = state["b"], state["a"]
+        state["pa"] = hb.flip(state["pa"])
+
+    for i in range(4):
+        one(i)
+    torch.cuda.synchronize()
+    sec = _time_steps(torch, one, 10)
+    cells = n * n  # targets alternate between 2048^2 (dual) and 2049^2 (primal); count the smaller
+    g = cells * dof_per_node(m, "cons") / sec / 1e9
+    tf = f_alg_cons(m) * cells / sec / 1e12
+    del par
+    return {"workload": "2D conservative Hermite m=5, 2048^2, Dirichlet x / Neumann y walls (C3)",
+            "gdof_per_s": g, "ms_per_step": sec * 1e3, "tflops_falg": tf, "frac_dmma_peak": tf / pk["dmma_tflops"],
+            "hbm_gbs": 24 * cells * dof_per_node(m, "cons") / sec / 1e9}
+
+
+def sweep(hb, torch, pk):
     """Config C4: dissipative m = 4..8 at ~2^30 DOF per level (device resident)."""
+    from paper_1802_05246_b200.stepping import diss2d_into
+
     out = {}
-    sizes = {2: 9088, 3: 6554, 4: 5118, 5: 4196, 6: 3554, 7: 3083, 8: 2721}
     for m in range(4, 9):
-        n = sizes[m]
+        n = SWEEP_N[m]
         grid = hb.Grid2D(0.0, 1.0, 0.0, 1.0, n, n, True)
         cfg = hb.SchemeConfig(m=m, lam=0.9)
         w = 2.0 * math.pi
         u = hb.standing_wave_on_grid(grid, hb.PRIMAL, 0.1, m, m, w, w, w * math.sqrt(2.0))
         v = hb.standing_wave_on_grid(grid, hb.PRIMAL, 0.1, m - 1, m - 1, w, w, w * math.sqrt(2.0), tder=1)
-        ud, vd = torch.empty_like(u), torch.empty_like(v)
-        from paper_1802_05246_b200.stepping import diss2d_into
-
+        bufs = [(u, v), (torch.empty_like(u), torch.empty_like(v))]
         bc = hb.BoundarySpec2D()
-        bufs = [(u, v), (ud, vd)]
-        par = hb.PRIMAL
-        for i in range(3):
-            diss2d_into(*bufs[i % 2], *bufs[(i + 1) % 2], grid, par, m, cfg, bc)
-            par = hb.flip(par)
+        st = {"par": hb.PRIMAL}
+
+        def one(i):
+            diss2d_into(*bufs[i % 2], *bufs[(i + 1) % 2], grid, st["par"], m, cfg, bc)
+            st["par"] = hb.flip(st["par"])
+
+        for i in range(2):
+            one(i)
         torch.cuda.synchronize()
-        k = 6
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for i in range(k):
-            diss2d_into(*bufs[(i + 3) % 2], *bufs[(i + 4) % 2], grid, par, m, cfg, bc)
-            par = hb.flip(par)
-        b.record()
-        torch.cuda.synchronize()
-        sec = a.elapsed_time(b) / 1e3 / k
+        sec = _time_steps(torch, lambda i: one(i + 2), 6)
         g = n * n * dof_per_node(m) / sec / 1e9
         tf = f_alg_diss(m) * n * n / sec / 1e12
+        dense, issued = cellmap_flops(m)
         out[f"m{m}"] = {"n": n, "gdof_per_s": g, "ms_per_step": sec * 1e3, "tflops_falg": tf,
-                        "frac_fp64": tf / p64, "hbm_gbs": 16 * n * n * dof_per_node(m) / sec / 1e9}
-        del u, v, ud, vd, bufs
+                        "frac_dmma_peak": tf / pk["dmma_tflops"],
+                        "issued_dmma_frac": issued * n * n / sec / 1e12 / pk["dmma_tflops"],
+                        "hbm_frac": 16 * n * n * dof_per_node(m) / sec / 1e9 / pk["hbm_gbs"]}
+        del u, v, bufs
         torch.cuda.empty_cache()
     return out
 

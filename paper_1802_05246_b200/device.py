@@ -55,14 +55,24 @@ class Staging:
                 raise ValueError("all fields of one call must live on the same device")
             return a.contiguous() if not a.is_contiguous() else a
         host = t.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
-        return host.to(self.device, non_blocking=False)
+        # pinned host memory (e.g. torch pin_memory buffers viewed as numpy)
+        # copies asynchronously on the current stream; pageable memory is
+        # staged by the driver and returns once copied
+        return host.to(self.device, non_blocking=True)
 
     def empty(self, shape):
         return torch().empty(tuple(int(s) for s in shape), dtype=torch().float64, device=self.device)
 
     def out(self, d):
+        """Device result -> caller's container.  Host results land in pinned
+        memory from torch's caching host allocator (fast DMA, no page faults
+        on reuse); the returned ndarray keeps that buffer alive."""
         if self.host:
-            return d.cpu().numpy()
+            t = torch()
+            h = t.empty(tuple(d.shape), dtype=d.dtype, pin_memory=True)
+            h.copy_(d, non_blocking=True)
+            t.cuda.current_stream(self.device).synchronize()
+            return h.numpy()
         return d
 
     @property
