@@ -49,8 +49,9 @@ def full_capture(rep):
     def num(k):
         val, unit = get.get(k, ("nan", ""))
         x = float(val.replace(",", ""))
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-                 "msecond": 1e-3}.get(unit, 1.0)
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6, "ms": 1e-3,
+                 "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "Ghz": 1e9, "Mhz": 1e6,
+                 "Kbyte/block": 1e3}.get(unit, 1.0)
         return x * scale
 
     out = {
