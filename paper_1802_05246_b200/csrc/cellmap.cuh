@@ -23,6 +23,8 @@
 
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "cellmap_shape.h"
 #include "common.cuh"
 
@@ -69,13 +71,17 @@ struct CMCfg {
   static constexpr int WBUF = KSC * NT * 32;
   static constexpr int SBUF = CBUF + WBUF;         // doubles per ring slot
   static constexpr int DO = O0 + O1;               // output record per cell
-  static constexpr int EPIB = NW * 8 * DO;         // per-warp epilogue staging (doubles)
-  static constexpr int PREVB = SCH == kCons ? NW * MT * 8 * O0 : 0;  // kCons: `previous` of the warp's cells
-  static constexpr int TAIL = (EPIB + PREVB) * 8 + NT * 8 * 4 + 64;
-  static constexpr int NS = (4 * SBUF * 8 + TAIL <= 227 * 1024) ? 4 : 3;  // ring depth
-  static constexpr int EPI0 = NS * SBUF;           // double offset of the staging slabs
+  // Per consumer warp: one output slab (its MT M-tiles' records, laid out as
+  // [8 x O0 | 8 x O1] per M-tile) drained to HBM by a producer warp, and for
+  // kCons one slab of `previous` records, staged at tile start.
+  static constexpr int SLAB = MT * 8 * DO;
+  static constexpr int PSLAB = SCH == kCons ? MT * 8 * O0 : 0;
+  static constexpr int EPIB = NW * (SLAB + PSLAB);
+  static constexpr int TAIL = EPIB * 8 + 32 * NT * 4 + (2 * 4 + 2 * NW) * 8 + 64;
+  static constexpr int NS = (4 * SBUF * 8 + TAIL <= 227 * 1024) ? 4 : ((3 * SBUF * 8 + TAIL <= 227 * 1024) ? 3 : 2);
+  static constexpr int EPI0 = NS * SBUF;           // double offset of the slabs
   static constexpr int SMEM = NS * SBUF * 8 + TAIL;
-  static constexpr bool UNROLL_KS = NT <= 9;       // fully unroll the k-steps of a chunk
+  static constexpr bool PREFETCH_B = NT <= 9;      // W fragments double-buffered in registers too
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -112,6 +118,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       : "memory");
 }
 
+// Non-blocking probe of a phase (warp-uniform when called by one lane and
+// broadcast).
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
+  unsigned ok = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
 // Producer-side wait: back off between polls so a producer that runs ahead
 // of the ring does not steal issue slots from the consumer warps.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) {
@@ -136,6 +158,13 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
       : "+d"(d[0]), "+d"(d[1])
       : "d"(a), "d"(b));
+}
+
+// D = A B (C = 0): the first k-step of a tile (no accumulator reset needed).
+__device__ __forceinline__ void dmma_first(double (&d)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%4};\n"
+      : "=d"(d[0]), "=d"(d[1])
+      : "d"(a), "d"(b), "d"(0.0));
 }
 
 __device__ __forceinline__ double flip_sign(double x, unsigned long long mask) {
@@ -172,18 +201,40 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
   constexpr int TR = C::TR, TJ = C::TJ, NT = C::NT, MT = C::MT, NS = C::NS, KSC = C::KSC, KC = C::KC,
                 KCP = C::KCP, NCH = C::NCH, NW = C::NW;
   extern __shared__ __align__(16) double smem[];
-  double* s_prev = smem + C::EPI0 + C::EPIB;
-  int* s_ocode = reinterpret_cast<int*>(smem + C::EPI0 + C::EPIB + C::PREVB);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::EPI0 + C::EPIB + C::PREVB + (NT * 8 + 1) / 2);
-  uint64_t* full = bars;        // [NS] producer -> consumers: slot staged
-  uint64_t* empty = bars + NS;  // [NS] consumers -> producer: slot consumed
+  double* slabs = smem + C::EPI0;                           // [NW][SLAB]
+  double* pslabs = slabs + NW * C::SLAB;                    // [NW][PSLAB]   (kCons)
+  unsigned* s_opos = reinterpret_cast<unsigned*>(pslabs + NW * C::PSLAB);  // [32][NT]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_opos + 32 * NT + (32 * NT) % 2);
+  uint64_t* full = bars;            // [NS] producers -> consumers: ring slot staged
+  uint64_t* empty = bars + 4;       // [NS] consumers -> producers: ring slot consumed
+  uint64_t* sfull = bars + 8;       // [NW] consumer w -> producer: output slab written
+  uint64_t* sempty = bars + 8 + NW; // [NW] producer -> consumer w: output slab drained
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  for (int i = tid; i < NT * 8; i += blockDim.x) s_ocode[i] = a.ocode[i];
+  // Slab position of each lane's two accumulator columns per n-tile, packed
+  // 16 + 16 bits (0xffff = padding): record order [8 x O0 | 8 x O1].
+  if (warp == 0) {
+    const int r = lane >> 2;
+    for (int nt = 0; nt < NT; ++nt) {
+      unsigned packed = 0;
+      for (int i = 0; i < 2; ++i) {
+        const int code = a.ocode[nt * 8 + (lane & 3) * 2 + i];
+        const unsigned pos = code < 0 ? 0xffffu
+                                      : (unsigned)((code >> 16) ? 8 * C::O0 + r * C::O1 + (code & 0xffff)
+                                                                : r * C::O0 + (code & 0xffff));
+        packed |= pos << (16 * i);
+      }
+      s_opos[lane * NT + nt] = packed;
+    }
+  }
   if (tid == 0) {
     for (int b = 0; b < NS; ++b) {
       mbar_init(&full[b], 2 * 32 * C::NPW);  // each producer lane: one plain arrive + one cp.async arrive
-      mbar_init(&empty[b], NW);  // one arrive per consumer warp
+      mbar_init(&empty[b], NW);               // one arrive per consumer warp
+    }
+    for (int w = 0; w < NW; ++w) {
+      mbar_init(&sfull[w], 1);
+      mbar_init(&sempty[w], 1);
     }
   }
   __syncthreads();
@@ -205,27 +256,99 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
     t.c_first = t.j0 + a.off;
     return t;
   };
+  // M-tile t of consumer warp w in tile `tg`: first target cell and valid count
+  auto mtile = [&](const CMTile& tg, int w, int t, int64_t& cell0) {
+    const int mt = w * MT + t;
+    const int trl = mt / (TJ / 8), jl0 = (mt % (TJ / 8)) * 8;
+    cell0 = (tg.tr0 + trl) * a.nty + tg.j0 + jl0;
+    return trl < tg.nvr ? (tg.nvc - jl0 < 8 ? tg.nvc - jl0 : 8) : 0;
+  };
 
   if (warp >= NW) {
     // ------------------------------------------------------------ producers
-    // producer lane pl -> entry e = pl % KC of the chunk, node columns q = pl / KC + QL k.
     constexpr int NPL = 32 * C::NPW;
     constexpr int QL = NPL / KC;
     constexpr int NQ = (TJ + QL) / QL;  // node columns per lane (ceil((TJ+1)/QL))
-    const int pl = tid - 32 * NW;
+    const int pl = tid - 32 * NW, pw = warp - NW;
     const int e = pl % KC, q0 = pl / KC;
+
+    // Output drain for consumer warps pw and pw + NPW: slab -> HBM, coalesced.
+    int dtile[NW / C::NPW], dk[NW / C::NPW];
+#pragma unroll
+    for (int j = 0; j < NW / C::NPW; ++j) dtile[j] = blockIdx.x, dk[j] = 0;
+    auto try_drain = [&]() {
+      bool any = false;
+#pragma unroll
+      for (int j = 0; j < NW / C::NPW; ++j) {
+        const int w = pw + C::NPW * j;
+        if (dtile[j] >= ntiles) continue;
+        int ready = lane == 0 ? (int)mbar_test(&sfull[w], dk[j] & 1) : 0;
+        ready = __shfl_sync(0xffffffffu, ready, 0);
+        if (!ready) continue;
+        const CMTile tg = tile_geo(dtile[j]);
+        const double* sl = slabs + w * C::SLAB;
+#pragma unroll
+        for (int t = 0; t < MT; ++t) {
+          int64_t cell0;
+          const int nv = mtile(tg, w, t, cell0);
+          if (MODE == 2 || nv == 0) continue;
+          double* o0 = a.out0 + cell0 * C::O0;
+          const double* s0 = sl + t * 8 * C::DO;
+          if (nv == 8) {  // full M-tile: fixed trip counts, all loads before the stores
+            constexpr int K0N = (8 * C::O0 + 31) / 32, K1N = (8 * C::O1 + 31) / 32;
+            double v0[K0N], v1[K1N > 0 ? K1N : 1];
+#pragma unroll
+            for (int kk = 0; kk < K0N; ++kk)
+              if (lane + 32 * kk < 8 * C::O0) v0[kk] = s0[lane + 32 * kk];
+#pragma unroll
+            for (int kk = 0; kk < K1N; ++kk)
+              if (lane + 32 * kk < 8 * C::O1) v1[kk] = s0[8 * C::O0 + lane + 32 * kk];
+#pragma unroll
+            for (int kk = 0; kk < K0N; ++kk)
+              if (lane + 32 * kk < 8 * C::O0) o0[lane + 32 * kk] = v0[kk];
+            if (C::O1 > 0) {
+              double* o1 = a.out1 + cell0 * C::O1;
+#pragma unroll
+              for (int kk = 0; kk < K1N; ++kk)
+                if (lane + 32 * kk < 8 * C::O1) o1[lane + 32 * kk] = v1[kk];
+            }
+          } else {
+            for (int q = lane; q < nv * C::O0; q += 32) o0[q] = s0[q];
+            if (C::O1 > 0) {
+              double* o1 = a.out1 + cell0 * C::O1;
+              for (int q = lane; q < nv * C::O1; q += 32) o1[q] = s0[8 * C::O0 + q];
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[w]);
+        dtile[j] += gridDim.x;
+        ++dk[j];
+        any = true;
+      }
+      return any;
+    };
+
     int tile = blockIdx.x, ch = 0;
     CMTile t = tile_geo(tile);
     for (int g = 0; g < nstages; ++g) {
       const int b = g % NS;
-      if (g >= NS) mbar_wait_sleep(&empty[b], ((g / NS) - 1) & 1);
+      if (g >= NS) {  // wait for the slot, draining finished output slabs meanwhile
+        while (true) {
+          int ok = lane == 0 ? (int)mbar_test(&empty[b], ((g / NS) - 1) & 1) : 0;
+          if (__shfl_sync(0xffffffffu, ok, 0)) break;
+          if (!try_drain()) __nanosleep(64);
+        }
+      } else {
+        try_drain();
+      }
       double* cb = smem + b * C::SBUF;
       const int slot = ch * KC + e;  // input slot: field 0 in [0, K0), field 1 in [K0, 4 NK)
       const bool f1 = slot >= C::K0;
       const int eo = f1 ? slot - C::K0 : slot;
       const bool pad = eo >= (f1 ? C::P1 : C::P0);
       const bool edge = t.s_first < 0 || t.s_first + t.nvr >= a.nx || t.c_first < 0 || t.c_first + t.nvc >= a.ny;
-      const bool manual = !a.periodic && edge;  // wall ghosts: load, reflect, store
+      const bool manual = !a.periodic && edge;  // wall ghosts: reflect after the copies land
       double* dst = cb + q0 * KCP + e;
       if (pad) {
 #pragma unroll 1
@@ -233,7 +356,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
 #pragma unroll
           for (int k = 0; k < NQ; ++k)
             if (q0 + k * QL <= TJ) dst[(r * (TJ + 1) + k * QL) * KCP] = 0.0;
-      } else if (MODE != 1 && t.nvr == TR && t.nvc == TJ && t.s_first >= a.f0.row0 &&
+      } else if (MODE != 1 && MODE != 3 && t.nvr == TR && t.nvc == TJ && t.s_first >= a.f0.row0 &&
                  t.s_first + TR < a.f0.row0 + a.f0.nrows && t.c_first >= 0 && t.c_first + TJ < a.ny) {
         // interior tile: every staged row is a dense segment of the local slab
         const int pf = f1 ? C::P1 : C::P0;
@@ -247,7 +370,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
             if (k < NQ - 1 || q0 + k * QL <= TJ) cm_cp_async8(dst + (r * (TJ + 1) + k * QL) * KCP, src + k * cstep);
           src += rowlen;
         }
-      } else if (MODE != 1) {
+      } else if (MODE != 1 && MODE != 3) {
         const int pf = f1 ? C::P1 : C::P0;
         const int64_t rowlen = a.ny * pf;
         int col[NQ];  // offset of this lane's entry in each staged column (fits 32 bits: ny * P < 2^31)
@@ -303,6 +426,14 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
         if (tile < ntiles) t = tile_geo(tile);
       }
     }
+    // drain the remaining output slabs
+    while (true) {
+      bool left = false;
+#pragma unroll
+      for (int j = 0; j < NW / C::NPW; ++j) left |= dtile[j] < ntiles;
+      if (!left) break;
+      if (!try_drain()) __nanosleep(64);
+    }
     return;
   }
 
@@ -322,116 +453,136 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
 #pragma unroll
     for (int n = 0; n < NT; ++n) acc[t][n][0] = acc[t][n][1] = 0.0;
 
-  int tile = blockIdx.x, ch = 0;
+  int tile = blockIdx.x, ch = 0, k = 0;  // k = this warp's tile count
   CMTile cg = tile_geo(tile);
-  double* st = smem + C::EPI0 + warp * 8 * C::DO;
+  double* slab = slabs + warp * C::SLAB;
   for (int g = 0; g < nstages; ++g) {
     const int b = g % NS;
     if (SCH == kCons && ch == 0) {
       // the epilogue subtracts `previous`: stage this warp's records (8 cells
       // x O0 doubles per M-tile, contiguous) with cp.async now, so they land
-      // while the tile's DMMAs run
+      // while the DMMAs run
+      double* pv = pslabs + warp * C::PSLAB;
 #pragma unroll
       for (int t = 0; t < MT; ++t) {
-        const int mt = warp * MT + t;
-        const int trl = mt / (TJ / 8), jl0 = (mt % (TJ / 8)) * 8;
-        const int nv = trl < cg.nvr ? (cg.nvc - jl0 < 8 ? cg.nvc - jl0 : 8) : 0;
-        const double* p = a.prev + ((cg.tr0 + trl) * a.nty + cg.j0 + jl0) * C::O0;
-        double* d = s_prev + (warp * MT + t) * 8 * C::O0;
-        for (int q = lane; q < nv * C::O0; q += 32) cm_cp_async8(d + q, p + q);
+        int64_t cell0;
+        const int nv = mtile(cg, warp, t, cell0);
+        const double* p = a.prev + cell0 * C::O0;
+        for (int q = lane; q < nv * C::O0; q += 32) cm_cp_async8(pv + t * 8 * C::O0 + q, p + q);
       }
     }
     mbar_wait(&full[b], (g / NS) & 1);
     const double* cb = smem + b * C::SBUF;
     const double* wb = cb + C::CBUF;
-    const int nks = (C::NK - ch * KSC) < KSC ? (C::NK - ch * KSC) : KSC;
-    auto kstep = [&](const int ks) {
-      const int step = ch * KSC + ks;
-      const unsigned long long mx = ((kxbits >> step) & 1ull) << 63;
-      const unsigned long long my = ((kybits >> step) & 1ull) << 63;
-      double A[MT][4];
+    // One chunk of NKS k-steps, software-pipelined: the shared-memory
+    // operands of k-step ks+1 (corner values; W fragments when registers
+    // allow) are loaded before the DMMAs of k-step ks issue.  FIRST: the
+    // tile's first chunk, whose first k-step starts the accumulators (C = 0).
+    auto run_chunk = [&](auto nks_c, auto first_c) {
+      constexpr int NKS = decltype(nks_c)::value;
+      constexpr bool FIRST = decltype(first_c)::value;
+      constexpr bool PREB = C::PREFETCH_B;
+      double raw[2][MT][4];
+      double bb[PREB ? 2 : 1][NT];
+      auto load = [&](const int ks, const int slot) {
 #pragma unroll
-      for (int t = 0; t < MT; ++t) {
-        const int mt = warp * MT + t;
-        const int trl = mt / (TJ / 8), tc = (mt % (TJ / 8)) * 8;
-        const double* p = cb + (trl * (TJ + 1) + tc + (lane >> 2)) * KCP + ks * 4 + (lane & 3);
-        const double c00 = p[0];
-        const double c01 = flip_sign(p[KCP], my);
-        const double c10 = flip_sign(p[(TJ + 1) * KCP], mx);
-        const double c11 = flip_sign(p[(TJ + 2) * KCP], mx ^ my);
-        const double ap = c00 + c10, am = c00 - c10, bp = c01 + c11, bm = c01 - c11;
-        A[t][0] = ap + bp;  // class (0,0)
-        A[t][1] = ap - bp;  // class (0,1)
-        A[t][2] = am + bm;  // class (1,0)
-        A[t][3] = am - bm;  // class (1,1)
-      }
-      const double* wk = wb + ks * NT * 32 + lane;
+        for (int t = 0; t < MT; ++t) {
+          const int mt = warp * MT + t;
+          const int trl = mt / (TJ / 8), tc = (mt % (TJ / 8)) * 8;
+          const double* p = cb + (trl * (TJ + 1) + tc + (lane >> 2)) * KCP + ks * 4 + (lane & 3);
+          raw[slot][t][0] = p[0];
+          raw[slot][t][1] = p[KCP];
+          raw[slot][t][2] = p[(TJ + 1) * KCP];
+          raw[slot][t][3] = p[(TJ + 2) * KCP];
+        }
+        if (PREB) {
+          const double* wk = wb + ks * NT * 32 + lane;
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int c = nt < C::B1 ? 0 : (nt < C::B2 ? 1 : (nt < C::B3 ? 2 : 3));  // parity class of tile nt
-        const double bf = wk[nt * 32];
+          for (int nt = 0; nt < NT; ++nt) bb[PREB ? slot : 0][nt] = wk[nt * 32];
+        }
+      };
+      load(0, 0);
 #pragma unroll
-        for (int t = 0; t < MT; ++t) dmma(acc[t][nt], A[t][c], bf);
+      for (int ks = 0; ks < NKS; ++ks) {
+        const int cur = ks & 1;
+        if (ks + 1 < NKS) load(ks + 1, cur ^ 1);
+        const int step = ch * KSC + ks;
+        const unsigned long long mx = ((kxbits >> step) & 1ull) << 63;
+        const unsigned long long my = ((kybits >> step) & 1ull) << 63;
+        double A[MT][4];
+#pragma unroll
+        for (int t = 0; t < MT; ++t) {
+          const double c00 = raw[cur][t][0];
+          const double c01 = flip_sign(raw[cur][t][1], my);
+          const double c10 = flip_sign(raw[cur][t][2], mx);
+          const double c11 = flip_sign(raw[cur][t][3], mx ^ my);
+          const double ap = c00 + c10, am = c00 - c10, bp = c01 + c11, bm = c01 - c11;
+          A[t][0] = ap + bp;  // class (0,0)
+          A[t][1] = ap - bp;  // class (0,1)
+          A[t][2] = am + bm;  // class (1,0)
+          A[t][3] = am - bm;  // class (1,1)
+        }
+        const double* wk = wb + ks * NT * 32 + lane;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int c = nt < C::B1 ? 0 : (nt < C::B2 ? 1 : (nt < C::B3 ? 2 : 3));  // parity class of tile nt
+          const double bf = PREB ? bb[PREB ? cur : 0][nt] : wk[nt * 32];
+#pragma unroll
+          for (int t = 0; t < MT; ++t) {
+            if (FIRST && ks == 0)
+              dmma_first(acc[t][nt], A[t][c], bf);
+            else
+              dmma(acc[t][nt], A[t][c], bf);
+          }
+        }
       }
     };
-    if constexpr (MODE == 2) {
-    } else if constexpr (C::UNROLL_KS) {
-#pragma unroll
-      for (int ks = 0; ks < KSC; ++ks)
-        if (ks < nks) kstep(ks);
-    } else {
-#pragma unroll 1
-      for (int ks = 0; ks < nks; ++ks) kstep(ks);
+    if constexpr (MODE != 2) {
+      using KF = std::integral_constant<int, KSC>;
+      using KL = std::integral_constant<int, C::NK - (NCH - 1) * KSC>;
+      if constexpr (NCH == 1) {
+        run_chunk(KL{}, std::true_type{});
+      } else {
+        if (ch == 0)
+          run_chunk(KF{}, std::true_type{});
+        else if (ch == NCH - 1)
+          run_chunk(KL{}, std::false_type{});
+        else
+          run_chunk(KF{}, std::false_type{});
+      }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[b]);  // slot b may be refilled
+    if (lane == 0) mbar_arrive(&empty[b]);  // ring slot b may be refilled
 
     if (ch == NCH - 1) {
-      // Epilogue, one M-tile at a time through this warp's staging slab, laid
-      // out exactly like the outputs: [8 records of field 0][8 records of
-      // field 1].  The fragments land at their record positions (ocode =
-      // field << 16 | offset, -1 = padding); the 8 cells' records, contiguous
-      // in each output field, are then written by consecutive lanes.
-      const int base0 = (lane >> 2) * C::O0, base1 = 8 * C::O0 + (lane >> 2) * C::O1;
-#pragma unroll
-      for (int t = 0; t < MT; ++t) {
-        const int mt = warp * MT + t;
-        const int trl = mt / (TJ / 8), jl0 = (mt % (TJ / 8)) * 8;
-        const int nv = trl < cg.nvr ? (cg.nvc - jl0 < 8 ? cg.nvc - jl0 : 8) : 0;
-#pragma unroll
-        for (int n = 0; n < NT; ++n)
-#pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const int code = s_ocode[n * 8 + (lane & 3) * 2 + i];
-            if (code >= 0) st[(code >> 16 ? base1 : base0) + (code & 0xffff)] = acc[t][n][i];
-            acc[t][n][i] = 0.0;
-          }
+      // Epilogue: accumulators -> this warp's output slab in record order; a
+      // producer warp drains the slab to HBM while this warp moves on.
+      if (k >= 1) mbar_wait(&sempty[warp], (k - 1) & 1);  // previous tile's slab drained
+      if (SCH == kCons) {  // `previous` landed (own copies), visible warp-wide after the fence
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
         __syncwarp();
-        if (SCH == kCons) asm volatile("cp.async.wait_all;\n" ::: "memory");
-        if (MODE != 2 && nv > 0) {
-          const int64_t cell0 = (cg.tr0 + trl) * a.nty + cg.j0 + jl0;
-          double* o0 = a.out0 + cell0 * C::O0;
-          const double* p0 = s_prev + (warp * MT + t) * 8 * C::O0;
+      }
+      const unsigned* op = s_opos + lane * NT;
+      const double* pv = pslabs + warp * C::PSLAB;
 #pragma unroll
-          for (int k = 0; k < (8 * C::O0 + 31) / 32; ++k) {
-            const int q = lane + 32 * k;
-            if (q < nv * C::O0) {
-              double v = st[q];
-              if (SCH == kCons) v -= p0[q];
-              o0[q] = v;
-            }
-          }
-          if (C::O1 > 0) {
-            double* o1 = a.out1 + cell0 * C::O1;
+      for (int n = 0; n < NT; ++n) {
+        const unsigned pk = op[n];
 #pragma unroll
-            for (int k = 0; k < (8 * C::O1 + 31) / 32; ++k) {
-              const int q = lane + 32 * k;
-              if (q < nv * C::O1) o1[q] = st[8 * C::O0 + q];
+        for (int i = 0; i < 2; ++i) {
+          const unsigned pos = (pk >> (16 * i)) & 0xffffu;
+          if (pos != 0xffffu) {
+#pragma unroll
+            for (int t = 0; t < MT; ++t) {
+              double v = acc[t][n][i];
+              if (SCH == kCons) v -= pv[t * 8 * C::O0 + pos];  // conservative.py:136 "- previous"
+              slab[t * 8 * C::DO + pos] = v;
             }
           }
         }
-        __syncwarp();
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sfull[warp]);
+      ++k;
       ch = 0;
       tile += gridDim.x;
       if (tile < ntiles) cg = tile_geo(tile);
