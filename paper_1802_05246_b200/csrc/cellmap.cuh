@@ -71,13 +71,15 @@ struct CMCfg {
   static constexpr int WBUF = KSC * NT * 32;
   static constexpr int SBUF = CBUF + WBUF;         // doubles per ring slot
   static constexpr int DO = O0 + O1;               // output record per cell
-  // Per consumer warp: one output slab (its MT M-tiles' records, laid out as
-  // [8 x O0 | 8 x O1] per M-tile) drained to HBM by a producer warp, and for
-  // kCons one slab of `previous` records, staged at tile start.
-  static constexpr int SLAB = MT * 8 * DO;
+  // Per consumer warp: one output slab holding its MT M-tiles' accumulators
+  // in DMMA fragment order ([t][nt][lane][2], conflict-free 16-byte stores),
+  // drained to HBM by a producer warp through the inverse map s_inv; for
+  // kCons one slab of `previous` records (record order), staged when the
+  // tile's last chunk starts and subtracted by the drain.
+  static constexpr int SLAB = MT * NT * 64;
   static constexpr int PSLAB = SCH == kCons ? MT * 8 * O0 : 0;
   static constexpr int EPIB = NW * (SLAB + PSLAB);
-  static constexpr int TAIL = EPIB * 8 + 32 * NT * 4 + (2 * 4 + 2 * NW) * 8 + 64;
+  static constexpr int TAIL = EPIB * 8 + (8 * DO + 8 * NT) * 4 + (2 * 4 + 2 * NW) * 8 + 64;
   static constexpr int NS = (4 * SBUF * 8 + TAIL <= 227 * 1024) ? 4 : ((3 * SBUF * 8 + TAIL <= 227 * 1024) ? 3 : 2);
   static constexpr int EPI0 = NS * SBUF;           // double offset of the slabs
   static constexpr int SMEM = NS * SBUF * 8 + TAIL;
@@ -203,28 +205,26 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
   extern __shared__ __align__(16) double smem[];
   double* slabs = smem + C::EPI0;                           // [NW][SLAB]
   double* pslabs = slabs + NW * C::SLAB;                    // [NW][PSLAB]   (kCons)
-  unsigned* s_opos = reinterpret_cast<unsigned*>(pslabs + NW * C::PSLAB);  // [32][NT]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_opos + 32 * NT + (32 * NT) % 2);
+  int* s_inv = reinterpret_cast<int*>(pslabs + NW * C::PSLAB);  // [8 * DO]: output -> fragment slot
+  int* s_ocode = s_inv + 8 * C::DO;                              // [NT * 8]: fragment column -> output
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_ocode + 8 * NT + (8 * C::DO + 8 * NT) % 2);
   uint64_t* full = bars;            // [NS] producers -> consumers: ring slot staged
   uint64_t* empty = bars + 4;       // [NS] consumers -> producers: ring slot consumed
   uint64_t* sfull = bars + 8;       // [NW] consumer w -> producer: output slab written
   uint64_t* sempty = bars + 8 + NW; // [NW] producer -> consumer w: output slab drained
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  // Slab position of each lane's two accumulator columns per n-tile, packed
-  // 16 + 16 bits (0xffff = padding): record order [8 x O0 | 8 x O1].
-  if (warp == 0) {
-    const int r = lane >> 2;
-    for (int nt = 0; nt < NT; ++nt) {
-      unsigned packed = 0;
-      for (int i = 0; i < 2; ++i) {
-        const int code = a.ocode[nt * 8 + (lane & 3) * 2 + i];
-        const unsigned pos = code < 0 ? 0xffffu
-                                      : (unsigned)((code >> 16) ? 8 * C::O0 + r * C::O1 + (code & 0xffff)
-                                                                : r * C::O0 + (code & 0xffff));
-        packed |= pos << (16 * i);
-      }
-      s_opos[lane * NT + nt] = packed;
+  // Inverse fragment map: output q of an M-tile's records, laid out
+  // [8 x O0 | 8 x O1], lives in fragment slot (nt * 32 + lane) * 2 + i, where
+  // lane = 4 r + j holds columns 2j, 2j+1 of n-tile nt for cell r.
+  for (int idx = tid; idx < NT * 8; idx += blockDim.x) {
+    const int nt = idx / 8, col = idx % 8, code = a.ocode[idx];
+    s_ocode[idx] = code;
+    if (code < 0) continue;
+    const int o = code & 0xffff;
+    for (int r = 0; r < 8; ++r) {
+      const int q = (code >> 16) ? 8 * C::O0 + r * C::O1 + o : r * C::O0 + o;
+      s_inv[q] = (nt * 32 + r * 4 + col / 2) * 2 + col % 2;
     }
   }
   if (tid == 0) {
@@ -287,22 +287,26 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
         if (!ready) continue;
         const CMTile tg = tile_geo(dtile[j]);
         const double* sl = slabs + w * C::SLAB;
+        const double* pl0 = pslabs + w * C::PSLAB;  // kCons: `previous`, record order
 #pragma unroll
         for (int t = 0; t < MT; ++t) {
           int64_t cell0;
           const int nv = mtile(tg, w, t, cell0);
           if (MODE == 2 || nv == 0) continue;
           double* o0 = a.out0 + cell0 * C::O0;
-          const double* s0 = sl + t * 8 * C::DO;
+          const double* s0 = sl + t * NT * 64;
           if (nv == 8) {  // full M-tile: fixed trip counts, all loads before the stores
             constexpr int K0N = (8 * C::O0 + 31) / 32, K1N = (8 * C::O1 + 31) / 32;
             double v0[K0N], v1[K1N > 0 ? K1N : 1];
 #pragma unroll
             for (int kk = 0; kk < K0N; ++kk)
-              if (lane + 32 * kk < 8 * C::O0) v0[kk] = s0[lane + 32 * kk];
+              if (lane + 32 * kk < 8 * C::O0) {
+                v0[kk] = s0[s_inv[lane + 32 * kk]];
+                if (SCH == kCons) v0[kk] -= pl0[t * 8 * C::O0 + lane + 32 * kk];  // conservative.py:136
+              }
 #pragma unroll
             for (int kk = 0; kk < K1N; ++kk)
-              if (lane + 32 * kk < 8 * C::O1) v1[kk] = s0[8 * C::O0 + lane + 32 * kk];
+              if (lane + 32 * kk < 8 * C::O1) v1[kk] = s0[s_inv[8 * C::O0 + lane + 32 * kk]];
 #pragma unroll
             for (int kk = 0; kk < K0N; ++kk)
               if (lane + 32 * kk < 8 * C::O0) o0[lane + 32 * kk] = v0[kk];
@@ -313,10 +317,11 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
                 if (lane + 32 * kk < 8 * C::O1) o1[lane + 32 * kk] = v1[kk];
             }
           } else {
-            for (int q = lane; q < nv * C::O0; q += 32) o0[q] = s0[q];
+            for (int q = lane; q < nv * C::O0; q += 32)
+              o0[q] = SCH == kCons ? s0[s_inv[q]] - pl0[t * 8 * C::O0 + q] : s0[s_inv[q]];
             if (C::O1 > 0) {
               double* o1 = a.out1 + cell0 * C::O1;
-              for (int q = lane; q < nv * C::O1; q += 32) o1[q] = s0[8 * C::O0 + q];
+              for (int q = lane; q < nv * C::O1; q += 32) o1[q] = s0[s_inv[8 * C::O0 + q]];
             }
           }
         }
@@ -458,17 +463,21 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
   double* slab = slabs + warp * C::SLAB;
   for (int g = 0; g < nstages; ++g) {
     const int b = g % NS;
-    if (SCH == kCons && ch == 0) {
-      // the epilogue subtracts `previous`: stage this warp's records (8 cells
-      // x O0 doubles per M-tile, contiguous) with cp.async now, so they land
-      // while the DMMAs run
-      double* pv = pslabs + warp * C::PSLAB;
+    if (ch == NCH - 1) {
+      // The tile's last chunk: the previous tile's slab must be drained before
+      // this tile's epilogue reuses it (and, for kCons, before its `previous`
+      // records are staged — contiguous, with cp.async, landing under the
+      // last chunk's DMMAs).
+      if (k >= 1) mbar_wait(&sempty[warp], (k - 1) & 1);
+      if (SCH == kCons) {
+        double* pv = pslabs + warp * C::PSLAB;
 #pragma unroll
-      for (int t = 0; t < MT; ++t) {
-        int64_t cell0;
-        const int nv = mtile(cg, warp, t, cell0);
-        const double* p = a.prev + cell0 * C::O0;
-        for (int q = lane; q < nv * C::O0; q += 32) cm_cp_async8(pv + t * 8 * C::O0 + q, p + q);
+        for (int t = 0; t < MT; ++t) {
+          int64_t cell0;
+          const int nv = mtile(cg, warp, t, cell0);
+          const double* p = a.prev + cell0 * C::O0;
+          for (int q = lane; q < nv * C::O0; q += 32) cm_cp_async8(pv + t * 8 * C::O0 + q, p + q);
+        }
       }
     }
     mbar_wait(&full[b], (g / NS) & 1);
@@ -555,31 +564,15 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
     if (lane == 0) mbar_arrive(&empty[b]);  // ring slot b may be refilled
 
     if (ch == NCH - 1) {
-      // Epilogue: accumulators -> this warp's output slab in record order; a
+      // Epilogue: accumulators -> this warp's output slab in fragment order; a
       // producer warp drains the slab to HBM while this warp moves on.
-      if (k >= 1) mbar_wait(&sempty[warp], (k - 1) & 1);  // previous tile's slab drained
-      if (SCH == kCons) {  // `previous` landed (own copies), visible warp-wide after the fence
-        asm volatile("cp.async.wait_all;\n" ::: "memory");
-        __syncwarp();
-      }
-      const unsigned* op = s_opos + lane * NT;
-      const double* pv = pslabs + warp * C::PSLAB;
 #pragma unroll
-      for (int n = 0; n < NT; ++n) {
-        const unsigned pk = op[n];
+      for (int t = 0; t < MT; ++t)
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const unsigned pos = (pk >> (16 * i)) & 0xffffu;
-          if (pos != 0xffffu) {
-#pragma unroll
-            for (int t = 0; t < MT; ++t) {
-              double v = acc[t][n][i];
-              if (SCH == kCons) v -= pv[t * 8 * C::O0 + pos];  // conservative.py:136 "- previous"
-              slab[t * 8 * C::DO + pos] = v;
-            }
-          }
-        }
-      }
+        for (int n = 0; n < NT; ++n)
+          *reinterpret_cast<double2*>(slab + t * NT * 64 + (n * 32 + lane) * 2) =
+              make_double2(acc[t][n][0], acc[t][n][1]);
+      if (SCH == kCons) asm volatile("cp.async.wait_all;\n" ::: "memory");  // `previous` landed
       __syncwarp();
       if (lane == 0) mbar_arrive(&sfull[warp]);
       ++k;
