@@ -58,29 +58,41 @@ struct CMCfg {
   static constexpr int KC = 4 * KSC;               // input slots per chunk
   static constexpr int NCH = (NK + KSC - 1) / KSC; // chunks per tile
   static constexpr int KCP = 20;                   // staged doubles per node (= 4 mod 16: conflict-free)
-  // 8-cell M-tiles per consumer warp: two (each W fragment feeds two DMMAs)
-  // while the accumulators fit the 168-register budget of 3 warps per SMSP
-  static constexpr int MT = NT <= 9 ? 2 : 1;
   static constexpr int NW = 8;                     // consumer warps
   static constexpr int NPW = 4;                    // producer warps (one per SM sub-partition)
   static constexpr int NTHREADS = 32 * (NW + NPW);
   static constexpr int TJ = 32;                    // target columns per tile
+  static constexpr int DO = O0 + O1;               // output record per cell
+  // setmaxnreg split of the 512 registers per lane of each SM sub-partition
+  // (2 consumer + NPW / 4 producer warps)
+  static constexpr int PREGS = NPW == 8 ? 56 : 72;
+  static constexpr int CREGS = ((512 - (NPW / 4) * PREGS) / 2) / 8 * 8 > 232 ? 232 : ((512 - (NPW / 4) * PREGS) / 2) / 8 * 8;
+  static constexpr int SMEM_MAX = 227 * 1024;
+  // Shared memory for MT M-tiles per consumer warp and an NS-slot ring:
+  //   ring slot = the tile's (2 MT + 1) x 33 staged nodes x KCP + 4 k-steps of W
+  //   per warp: one output slab in DMMA fragment order ([t][nt][lane][2],
+  //   conflict-free 16-byte stores; drained by the producers through the
+  //   inverse map s_inv) and, for kCons, one slab of `previous` records.
+  static constexpr int sbuf(int mt) { return (NW * mt / (TJ / 8) + 1) * (TJ + 1) * KCP + KSC * NT * 32; }
+  static constexpr int tail(int mt) {
+    return NW * (mt * NT * 64 + (SCH == kCons ? mt * 8 * O0 : 0)) * 8 + (8 * DO + 8 * NT) * 4 + (8 + 2 * NW) * 8 + 64;
+  }
+  static constexpr bool fits(int mt, int ns) { return ns * sbuf(mt) * 8 + tail(mt) <= SMEM_MAX; }
+  // 8-cell M-tiles per consumer warp.  Each staged W fragment feeds MT DMMAs
+  // and each corner load feeds NT, so shared-memory traffic per DMMA falls as
+  // (4 MT + NT) / (MT NT): take MT = 2 where its accumulators (2 MT NT
+  // doubles) fit the consumer registers and its slabs fit beside a 2-slot ring.
+  // (MT = 3 measured slower than 2 at m = 4: the ring shrinks to 3 slots.)
+  static constexpr int MT = (2 * NT <= 32 && fits(2, 2)) ? 2 : 1;
   static constexpr int TR = NW * MT / (TJ / 8);    // target rows per tile
   static constexpr int NODES = (TR + 1) * (TJ + 1);
   static constexpr int CBUF = NODES * KCP;
   static constexpr int WBUF = KSC * NT * 32;
   static constexpr int SBUF = CBUF + WBUF;         // doubles per ring slot
-  static constexpr int DO = O0 + O1;               // output record per cell
-  // Per consumer warp: one output slab holding its MT M-tiles' accumulators
-  // in DMMA fragment order ([t][nt][lane][2], conflict-free 16-byte stores),
-  // drained to HBM by a producer warp through the inverse map s_inv; for
-  // kCons one slab of `previous` records (record order), staged when the
-  // tile's last chunk starts and subtracted by the drain.
   static constexpr int SLAB = MT * NT * 64;
   static constexpr int PSLAB = SCH == kCons ? MT * 8 * O0 : 0;
-  static constexpr int EPIB = NW * (SLAB + PSLAB);
-  static constexpr int TAIL = EPIB * 8 + (8 * DO + 8 * NT) * 4 + (2 * 4 + 2 * NW) * 8 + 64;
-  static constexpr int NS = (4 * SBUF * 8 + TAIL <= 227 * 1024) ? 4 : ((3 * SBUF * 8 + TAIL <= 227 * 1024) ? 3 : 2);
+  static constexpr int TAIL = tail(MT);
+  static constexpr int NS = fits(MT, 4) ? 4 : (fits(MT, 3) ? 3 : 2);  // ring depth
   static constexpr int EPI0 = NS * SBUF;           // double offset of the slabs
   static constexpr int SMEM = NS * SBUF * 8 + TAIL;
   static constexpr bool PREFETCH_B = NT <= 9;      // W fragments double-buffered in registers too
@@ -266,6 +278,8 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
 
   if (warp >= NW) {
     // ------------------------------------------------------------ producers
+    // one warpgroup; hands registers to the consumer warpgroups
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::PREGS));
     constexpr int NPL = 32 * C::NPW;
     constexpr int QL = NPL / KC;
     constexpr int NQ = (TJ + QL) / QL;  // node columns per lane (ceil((TJ+1)/QL))
@@ -295,26 +309,41 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
           if (MODE == 2 || nv == 0) continue;
           double* o0 = a.out0 + cell0 * C::O0;
           const double* s0 = sl + t * NT * 64;
-          if (nv == 8) {  // full M-tile: fixed trip counts, all loads before the stores
+          if (nv == 8) {  // full M-tile: fixed trip counts, loads batched 4 ahead of the stores
             constexpr int K0N = (8 * C::O0 + 31) / 32, K1N = (8 * C::O1 + 31) / 32;
-            double v0[K0N], v1[K1N > 0 ? K1N : 1];
 #pragma unroll
-            for (int kk = 0; kk < K0N; ++kk)
-              if (lane + 32 * kk < 8 * C::O0) {
-                v0[kk] = s0[s_inv[lane + 32 * kk]];
-                if (SCH == kCons) v0[kk] -= pl0[t * 8 * C::O0 + lane + 32 * kk];  // conservative.py:136
+            for (int k0 = 0; k0 < K0N; k0 += 4) {
+              double v[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int q = lane + 32 * (k0 + u);
+                if (k0 + u < K0N && q < 8 * C::O0) {
+                  v[u] = s0[s_inv[q]];
+                  if (SCH == kCons) v[u] -= pl0[t * 8 * C::O0 + q];  // conservative.py:136
+                }
               }
 #pragma unroll
-            for (int kk = 0; kk < K1N; ++kk)
-              if (lane + 32 * kk < 8 * C::O1) v1[kk] = s0[s_inv[8 * C::O0 + lane + 32 * kk]];
-#pragma unroll
-            for (int kk = 0; kk < K0N; ++kk)
-              if (lane + 32 * kk < 8 * C::O0) o0[lane + 32 * kk] = v0[kk];
+              for (int u = 0; u < 4; ++u) {
+                const int q = lane + 32 * (k0 + u);
+                if (k0 + u < K0N && q < 8 * C::O0) o0[q] = v[u];
+              }
+            }
             if (C::O1 > 0) {
               double* o1 = a.out1 + cell0 * C::O1;
 #pragma unroll
-              for (int kk = 0; kk < K1N; ++kk)
-                if (lane + 32 * kk < 8 * C::O1) o1[lane + 32 * kk] = v1[kk];
+              for (int k0 = 0; k0 < K1N; k0 += 4) {
+                double v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  const int q = lane + 32 * (k0 + u);
+                  if (k0 + u < K1N && q < 8 * C::O1) v[u] = s0[s_inv[8 * C::O0 + q]];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  const int q = lane + 32 * (k0 + u);
+                  if (k0 + u < K1N && q < 8 * C::O1) o1[q] = v[u];
+                }
+              }
             }
           } else {
             for (int q = lane; q < nv * C::O0; q += 32)
@@ -443,6 +472,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
   }
 
   // -------------------------------------------------------------- consumers
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(C::CREGS));
   // Parity bits (kx & 1, ky & 1) of this lane's input slot 4 s + (lane & 3)
   // at every k-step s (sign flips of the x- / y-right corners).
   unsigned long long kxbits = 0, kybits = 0;
