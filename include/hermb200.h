@@ -174,6 +174,26 @@ int hw_l2err1d(const double* src, int mu, int64_t n_src, int parity_src,
                const double* xi, const double* w, const double* ex,
                double* out_host, void* stream);
 
+/*
+ * diagnostics.py:201-212 seminorm_sq of the global interpolant of a 1D field
+ * (pieces = cells of the field's own gather, ghosts with the bc's values as
+ * field_interpolant does): scale * sum over pieces of the Gauss integral
+ * (npts points, nodes gx / weights gw on [-1, 1], host pointers) of the squared
+ * order-th derivative.  dissipative_energy (diagnostics.py:229-234) is
+ * c^2 |I_m u|^2_{m+1} + |I_{m-1} v|^2_m, i.e. two calls.
+ */
+int hw_seminorm1d(const double* f, int mu, int64_t n_src, int parity, const hw_axis_bc* bc, double h, int order,
+                  double scale, int npts, const double* gx, const double* gw, double* out_host, void* stream);
+
+/*
+ * diagnostics.py:190-226 conservative_energy on a periodic grid:
+ * |P+|^2_{m+1} + |P-|^2_{m+1}, P± = p(cur) - p(prev)(x ± delta), delta =
+ * c dt / 2 (< h), integrated exactly on the union pieces with npts = m + 1
+ * Gauss points (host pointers gx, gw).  cur has parity_cur, prev the opposite.
+ */
+int hw_cons_energy1d(const double* cur, const double* prev, int m, int64_t n_src, int parity_cur, double h,
+                     double delta, int npts, const double* gx, const double* gw, double* out_host, void* stream);
+
 /* driver.py:259-262 _require_finite: *nonfinite_host = count of non-finite. */
 int hw_count_nonfinite(const double* a, int64_t n, int64_t* nonfinite_host,
                        void* stream);

@@ -421,6 +421,68 @@ def l2_error_1d(values, parity, n, periodic, x_left, h, exact, npts=None, bc=PER
     return math.sqrt(total)
 
 
+# ----------------------------------------------------------------- energies (1D)
+
+def _deriv(coeffs, order, h):
+    """poly.py:56-74 CellPolynomial.derivative on a (pieces, L) coefficient array."""
+    n = coeffs.shape[-1] - order
+    if n <= 0:
+        return np.zeros(coeffs.shape[:-1] + (1,))
+    fall = np.array([math.factorial(j + order) // math.factorial(j) for j in range(n)], dtype=float)
+    return coeffs[..., order:] * fall / h**order
+
+
+def _horner_cols(d, xi):
+    """Evaluate pieces d (P, L) at points xi (P, Q) or (Q,)."""
+    out = np.zeros(np.broadcast(d[:, :1], xi).shape) + d[:, -1:]
+    for j in range(d.shape[-1] - 2, -1, -1):
+        out = out * xi + d[:, j:j + 1]
+    return out
+
+
+def seminorm_sq_1d(values, parity, n, periodic, h, order, bc=PERIODIC_BC):
+    """diagnostics.py:201-212 over field_interpolant's pieces (diagnostics.py:47-59)."""
+    d = _deriv(interp_1d(pair_data(values, parity, periodic, bc)), order, h)
+    xg, wg = np.polynomial.legendre.leggauss(d.shape[-1])
+    q = _horner_cols(d, 0.5 * xg[None, :])
+    return float(np.sum(0.5 * h * (q * q) @ wg))
+
+
+def dissipative_energy_1d(u, v, parity, n, periodic, h, speed, bc=PERIODIC_BC):
+    """diagnostics.py:229-234."""
+    m = u.shape[1] - 1
+    return speed * speed * seminorm_sq_1d(u, parity, n, periodic, h, m + 1, bc) + \
+        seminorm_sq_1d(v, parity, n, periodic, h, m, bc)
+
+
+def conservative_energy_1d(cur, prev, parity_cur, n, h, delta):
+    """diagnostics.py:190-226 on a periodic grid, restated per union piece.
+
+    Cur piece t spans its two source nodes; the prev pieces shifted by
+    -/+delta that meet it are the ones centred on those nodes, split at
+    xi = -/+delta/h (pp_subtract's merged breakpoints).  Both (m+1)-th
+    derivatives are evaluated in their own scaled variables at m+1 Gauss
+    points per union piece (exact for the degree-2m integrand)."""
+    m = cur.shape[1] - 1
+    off = 0 if parity_cur == PRIMAL else -1
+    dc = _deriv(interp_1d(pair_data(cur, parity_cur, True, PERIODIC_BC)), m + 1, h)
+    dp = _deriv(interp_1d(pair_data(prev, flip(parity_cur), True, PERIODIC_BC)), m + 1, h)
+    t = np.arange(n)
+    dl, dr = dp[(t + off) % n], dp[(t + off + 1) % n]
+    xg, wg = np.polynomial.legendre.leggauss(m + 1)
+    dx = delta / h
+    total = 0.0
+    for sgn in (1, -1):
+        xs = -sgn * dx
+        for lo, hi, dpp, shp in ((-0.5, xs, dl, sgn * dx + 0.5), (xs, 0.5, dr, sgn * dx - 0.5)):
+            if hi <= lo:
+                continue
+            xi = 0.5 * (lo + hi) + 0.5 * (hi - lo) * xg
+            q = _horner_cols(dc, xi[None, :]) - _horner_cols(dpp, xi[None, :] + shp)
+            total += float(np.sum(0.5 * (hi - lo) * h * (q * q) @ wg))
+    return total
+
+
 # ----------------------------------------------------------------- driver.py data
 
 def scale_cols(vals, h):

@@ -586,6 +586,89 @@ int hw_l2err1d(const double* src, int mu, int64_t n_src, int parity_src, const h
   });
 }
 
+static Energy1DArgs energy_args(int mu, int64_t n_src, int parity, const hw_axis_bc* bc, double h, int npts,
+                                const double* gx, const double* gw) {
+  HW_CHECK(bc, "null boundary spec");
+  HW_CHECK(mu >= 0 && mu <= kMax1D, "order out of range");
+  HW_CHECK(npts >= 1 && npts <= 64 && gx && gw, "bad Gauss rule");
+  const int periodic = bc->left_kind == HW_PERIODIC;
+  check_bc_axis(*bc, periodic);
+  HW_CHECK(parity == HW_PRIMAL || parity == HW_DUAL, "unknown parity");
+  Energy1DArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.n = n_src;
+  a.nt = target_count(n_src, parity, periodic);
+  HW_CHECK(n_src >= 1 && a.nt >= 1, "grid too small");
+  a.off = src_offset(parity);
+  a.periodic = periodic;
+  a.kl = periodic ? 0 : bc->left_kind;
+  a.kh = periodic ? 0 : bc->right_kind;
+  a.gl = bc->left_value;
+  a.gh = bc->right_value;
+  a.mu = mu;
+  a.h = h;
+  a.npts = npts;
+  a.hl = device_hl(mu);
+  return a;
+}
+
+// Gauss rule (host arrays) -> device copies owned by the caller's DevBufs.
+static void upload_rule(Energy1DArgs& a, const double* gx, const double* gw, DevBuf& dx, DevBuf& dw) {
+  cuda_check(cudaMalloc(&dx.p, a.npts * 8), "cudaMalloc");
+  cuda_check(cudaMalloc(&dw.p, a.npts * 8), "cudaMalloc");
+  cuda_check(cudaMemcpy(dx.p, gx, a.npts * 8, cudaMemcpyHostToDevice), "cudaMemcpy");
+  cuda_check(cudaMemcpy(dw.p, gw, a.npts * 8, cudaMemcpyHostToDevice), "cudaMemcpy");
+  a.gx = dx.p;
+  a.gw = dw.p;
+}
+
+int hw_seminorm1d(const double* f, int mu, int64_t n_src, int parity, const hw_axis_bc* bc, double h, int order,
+                  double scale, int npts, const double* gx, const double* gw, double* out_host, void* stream) {
+  return guard([&] {
+    HW_CHECK(f && out_host, "null pointer");
+    HW_CHECK(order >= 0, "derivative order must be nonnegative");
+    Energy1DArgs a = energy_args(mu, n_src, parity, bc, h, npts, gx, gw);
+    a.f = f;
+    a.order = order;
+    a.scale = scale;
+    DevBuf dx, dw;
+    upload_rule(a, gx, gw, dx, dw);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t nblk = (a.nt + kRedThreads - 1) / kRedThreads;
+    DevBuf part;
+    cuda_check(cudaMalloc(&part.p, nblk * 8), "cudaMalloc");
+    a.part = part.p;
+    seminorm1d_kernel<<<(unsigned)nblk, kRedThreads, 0, st>>>(a);
+    cuda_check(cudaGetLastError(), "seminorm1d launch");
+    *out_host = reduce_partials(part.p, nblk, st);
+  });
+}
+
+int hw_cons_energy1d(const double* cur, const double* prev, int m, int64_t n_src, int parity_cur, double h,
+                     double delta, int npts, const double* gx, const double* gw, double* out_host, void* stream) {
+  return guard([&] {
+    HW_CHECK(cur && prev && out_host, "null pointer");
+    hw_axis_bc per = {HW_PERIODIC, HW_PERIODIC, 0.0, 0.0};
+    Energy1DArgs a = energy_args(m, n_src, parity_cur, &per, h, npts, gx, gw);
+    HW_CHECK(delta >= 0.0 && delta < h, "shift distance must be smaller than the smallest cell");
+    a.f = cur;
+    a.g = prev;
+    a.offg = src_offset(parity_cur == HW_PRIMAL ? HW_DUAL : HW_PRIMAL);
+    a.order = m + 1;
+    a.delta = delta;
+    DevBuf dx, dw;
+    upload_rule(a, gx, gw, dx, dw);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t nblk = (a.nt + kRedThreads - 1) / kRedThreads;
+    DevBuf part;
+    cuda_check(cudaMalloc(&part.p, nblk * 8), "cudaMalloc");
+    a.part = part.p;
+    cons_energy1d_kernel<<<(unsigned)nblk, kRedThreads, 0, st>>>(a);
+    cuda_check(cudaGetLastError(), "cons_energy1d launch");
+    *out_host = reduce_partials(part.p, nblk, st);
+  });
+}
+
 int hw_count_nonfinite(const double* x, int64_t n, int64_t* out_host, void* stream) {
   return guard([&] {
     HW_CHECK(out_host, "null output");

@@ -3,6 +3,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "line1d.cuh"
 
 namespace hw {
 
@@ -230,6 +231,131 @@ __global__ void init2d_kernel(Init2DArgs a) {
       }
     }
   }
+}
+
+}  // namespace hw
+
+namespace hw {
+
+// ------------------------------------------------------------------ 1D energies
+// diagnostics.py:201-234.  Pieces are the cells of the field's own gather
+// (field_interpolant, diagnostics.py:47-59): piece t interpolates the flanking
+// source nodes of target t, centred at the target node, width h.
+struct Energy1DArgs {
+  const double* f;       // field (order mu) / kCons: current level (order m)
+  const double* g;       // kCons: previous level (opposite parity, order m)
+  int64_t n, nt;         // source nodes, pieces
+  int off, offg;         // gather offsets of f's and g's parities
+  int periodic, kl, kh;
+  double gl, gh;
+  int mu, order;         // interpolation order, derivative order
+  double h, scale, delta;
+  int npts;
+  const double* gx;      // Gauss nodes / weights on [-1, 1]
+  const double* gw;
+  const double* hl;      // HL_mu
+  double* part;
+};
+
+// Coefficients of the order-th derivative of the piece polynomial in its
+// scaled variable xi = (x - centre)/h, including the 1/h^order factor
+// (poly.py:56-74): d_j = c_{j+r} (j+r)!/j! / h^r.
+__host__ __device__ inline int deriv_coeffs(const double* c, int ncoef, int r, double h, double* d) {
+  const int nd = ncoef - r;
+  double hr = 1.0;
+  for (int q = 0; q < r; ++q) hr *= h;
+  for (int j = 0; j < nd; ++j) {
+    double fall = 1.0;
+    for (int q = j + 1; q <= j + r; ++q) fall *= q;
+    d[j] = c[j + r] * fall / hr;
+  }
+  return nd;
+}
+
+__host__ __device__ inline double horner(const double* d, int nd, double x) {
+  double v = d[nd - 1];
+  for (int j = nd - 2; j >= 0; --j) v = v * x + d[j];
+  return v;
+}
+
+__host__ __device__ inline void piece_coeffs(const double* f, int mu, int64_t t, int off, const Energy1DArgs& a, double* c) {
+  Line1DArgs la;
+  la.n = a.n;
+  la.off = off;
+  la.periodic = a.periodic;
+  la.kl = a.kl;
+  la.kh = a.kh;
+  double L[kMax1D + 1], R[kMax1D + 1];
+  load_pair(f, mu, t, la, a.gl, a.gh, L, R);
+  interp1d(a.hl, mu, L, R, c);
+}
+
+// seminorm_sq (diagnostics.py:201-212): sum over pieces of the Gauss integral
+// of the squared order-th derivative over [centre - h/2, centre + h/2].
+__global__ void seminorm1d_kernel(Energy1DArgs a) {
+  __shared__ double sh[kRedThreads];
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double local = 0.0;
+  if (t < a.nt) {
+    double c[2 * kMax1D + 2], d[2 * kMax1D + 2];
+    piece_coeffs(a.f, a.mu, t, a.off, a, c);
+    const int nd = deriv_coeffs(c, 2 * a.mu + 2, a.order, a.h, d);
+    if (nd > 0) {
+      for (int p = 0; p < a.npts; ++p) {
+        const double q = horner(d, nd, 0.5 * a.gx[p]);
+        local += 0.5 * a.h * a.gw[p] * q * q;
+      }
+    }
+  }
+  const double bs = block_sum(local * a.scale, sh);
+  if (threadIdx.x == 0) a.part[blockIdx.x] = bs;
+}
+
+// conservative_energy (diagnostics.py:190-226) on a periodic grid:
+// E = |P+|^2_{m+1} + |P-|^2_{m+1}, P± = cur - S± prev, S± w(x) = w(x ± delta).
+// Within cur piece t (edges at its flanking source nodes) the shifted prev
+// pieces are the ones centred on those two nodes, split at xi_s = -/+ delta/h:
+// every union piece (pp_subtract's merged breakpoints) lies in one cur and one
+// prev piece, and both derivatives are evaluated in their own scaled
+// variables at the union piece's Gauss points (npts = m + 1: exact).
+__host__ __device__ inline double cons_energy_piece(const Energy1DArgs& a, int64_t t) {
+  const int m = a.mu, K = 2 * m + 2;
+  double cc[2 * kMax1D + 2], cl[2 * kMax1D + 2], cr[2 * kMax1D + 2];
+  double dc[2 * kMax1D + 2], dl[2 * kMax1D + 2], dr[2 * kMax1D + 2];
+  // prev pieces centred on cur piece t's left / right source nodes
+  const int64_t sl = pmod(t + a.off, a.n), sr = pmod(t + a.off + 1, a.n);
+  piece_coeffs(a.f, m, t, a.off, a, cc);
+  piece_coeffs(a.g, m, sl, a.offg, a, cl);
+  piece_coeffs(a.g, m, sr, a.offg, a, cr);
+  const int nd = deriv_coeffs(cc, K, m + 1, a.h, dc);
+  deriv_coeffs(cl, K, m + 1, a.h, dl);
+  deriv_coeffs(cr, K, m + 1, a.h, dr);
+  const double dx = a.delta / a.h;
+  double local = 0.0;
+  for (int sgn = 1; sgn >= -1; sgn -= 2) {  // P+ evaluates prev at x + delta, P- at x - delta
+    const double xs = -sgn * dx;            // split point in cur's scaled variable
+    for (int piece = 0; piece < 2; ++piece) {
+      const double lo = piece ? xs : -0.5, hi = piece ? 0.5 : xs;
+      if (hi <= lo) continue;
+      const double* dp = piece ? dr : dl;
+      const double sh_p = sgn * dx + (piece ? -0.5 : 0.5);  // xi_prev = xi + sh_p
+      for (int p = 0; p < a.npts; ++p) {
+        const double xi = 0.5 * (lo + hi) + 0.5 * (hi - lo) * a.gx[p];
+        const double q = horner(dc, nd, xi) - horner(dp, nd, xi + sh_p);
+        local += 0.5 * (hi - lo) * a.h * a.gw[p] * q * q;
+      }
+    }
+  }
+  return local;
+}
+
+__global__ void cons_energy1d_kernel(Energy1DArgs a) {
+  __shared__ double sh[kRedThreads];
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const double local = t < a.nt ? cons_energy_piece(a, t) : 0.0;
+  const double bs = block_sum(local, sh);
+
+  if (threadIdx.x == 0) a.part[blockIdx.x] = bs;
 }
 
 }  // namespace hw

@@ -30,7 +30,7 @@ struct Line1DArgs {
 };
 
 // Flanking data of target t: left/right source nodes with ghosts.
-__device__ inline void load_pair(const double* f, int mu, int64_t t, const Line1DArgs& a, double gl,
+__host__ __device__ inline void load_pair(const double* f, int mu, int64_t t, const Line1DArgs& a, double gl,
                                  double gh, double* L, double* R) {
   const int64_t s0 = t + a.off;
 #pragma unroll 1
@@ -65,7 +65,7 @@ __device__ inline void load_pair(const double* f, int mu, int64_t t, const Line1
 
 // Interpolant coefficients c[0..2mu+1] from (L, R) via the left block:
 // c[a] = sum_k HL[a][k] (L[k] + (-1)^(a+k) R[k])   (interp.py:78-90)
-__device__ inline void interp1d(const double* hl, int mu, const double* L, const double* R, double* c) {
+__host__ __device__ inline void interp1d(const double* hl, int mu, const double* L, const double* R, double* c) {
   for (int a = 0; a < 2 * mu + 2; ++a) {
     double s = 0.0;
     for (int k = 0; k <= mu; ++k) {

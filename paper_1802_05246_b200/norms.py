@@ -177,6 +177,65 @@ def l2_errors_pair(pair: FieldPair, exact_u, exact_dux, exact_v, bc: BoundarySpe
     return (_l2_1d(pair.u, bc, qu, 0, st), _l2_1d(pair.u, bc, qd, 1, st), _l2_1d(pair.v, bc, qv, 0, st))
 
 
+# ---------------------------------------------------------------- energies (1D)
+
+def _seminorm_sq(field: Field1D, bc: BoundarySpec, order: int, scale: float, st: Staging) -> float:
+    """scale * |I field|^2_order on the field's own pieces (diagnostics.py:201-212)."""
+    grid = field.grid
+    check_periodicity(bc, grid.periodic)
+    nd = 2 * field.order + 2 - order  # coefficients of the order-th derivative
+    if nd <= 0:
+        return 0.0
+    xg, wg = gauss_rule(nd)  # seminorm_sq integrates with deg + 1 points
+    gx = np.ascontiguousarray(xg, dtype=np.float64)
+    gw = np.ascontiguousarray(wg, dtype=np.float64)
+    f = st.to_dev(field.values)
+    abc = L.axis_bc(bc)
+    out = C.c_double(0.0)
+    L.check(L.lib().hw_seminorm1d(ptr(f), int(field.order), grid.n_nodes(field.parity), _PARITY[field.parity],
+                                  C.byref(abc), grid.h, int(order), float(scale), int(nd),
+                                  gx.ctypes.data_as(C.c_void_p), gw.ctypes.data_as(C.c_void_p), C.byref(out),
+                                  st.stream), "seminorm_sq")
+    return out.value
+
+
+def dissipative_energy(state: FieldPair, speed: float, bc: BoundarySpec) -> float:
+    """c^2 |I_m u|_{m+1}^2 + |I_{m-1} v|_m^2 (diagnostics.py:229-234), on the device."""
+    m = state.u.order
+    st = Staging(state.u.values, state.v.values)
+    return (_seminorm_sq(state.u, bc, m + 1, speed * speed, st) + _seminorm_sq(state.v, bc, m, 1.0, st))
+
+
+def conservative_energy(current: Field1D, previous: Field1D, speed: float, dt: float, bc: BoundarySpec) -> float:
+    """E(t_n) = |P+|^2_{m+1} + |P-|^2_{m+1} of a two-level state (diagnostics.py:190-226).
+
+    P± = p^n - S± p^{n-1/2}, S± w(x) = w(x ± c dt/2), integrated exactly on the
+    union pieces; periodic grids only, like the reference."""
+    grid = current.grid
+    check_periodicity(bc, grid.periodic)
+    if not (grid.periodic and previous.grid.periodic):
+        raise ValueError("conserved variables need a periodic domain")
+    if current.parity == previous.parity:
+        raise ValueError("the two levels must sit on opposite parities")
+    m = current.order
+    if previous.order != m:
+        raise ValueError(f"levels carry orders {m} and {previous.order}")
+    delta = 0.5 * speed * dt
+    if abs(delta) >= grid.h:  # poly.py:223-224
+        raise ValueError("shift distance must be smaller than the smallest cell")
+    xg, wg = gauss_rule(m + 1)
+    gx = np.ascontiguousarray(xg, dtype=np.float64)
+    gw = np.ascontiguousarray(wg, dtype=np.float64)
+    st = Staging(current.values, previous.values)
+    c = st.to_dev(current.values)
+    p = st.to_dev(previous.values)
+    out = C.c_double(0.0)
+    L.check(L.lib().hw_cons_energy1d(ptr(c), ptr(p), int(m), grid.n_nodes(current.parity), _PARITY[current.parity],
+                                     grid.h, abs(delta), int(m + 1), gx.ctypes.data_as(C.c_void_p),
+                                     gw.ctypes.data_as(C.c_void_p), C.byref(out), st.stream), "conservative_energy")
+    return out.value
+
+
 @dataclass(frozen=True)
 class ErrorReport:
     """Refinement-study results, coarsest first (diagnostics.py:241-270)."""
@@ -214,4 +273,5 @@ def fit_rate(hs, errors) -> float:
 
 
 __all__ = ["gauss_rule", "default_npts", "PlaneWave2D", "StandingWave2D", "l2_error_field_2d",
-           "l2_error_field", "l2_errors_pair", "ErrorReport", "fit_rate", "PRIMAL", "DUAL"]
+           "l2_error_field", "l2_errors_pair", "dissipative_energy", "conservative_energy", "ErrorReport",
+           "fit_rate", "PRIMAL", "DUAL"]
