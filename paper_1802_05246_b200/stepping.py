@@ -64,6 +64,66 @@ def diss2d_into(u, v, ud, vd, grid, parity, m, cfg: SchemeConfig, bc: BoundarySp
     return dt
 
 
+def _diss2d_host_pipelined(uh, vh, grid, parity, m, cfg: SchemeConfig, bc: BoundarySpec2D, nchunks: int = 8):
+    """Host arrays in, host arrays out, with the PCIe traffic overlapped: the
+    source rows go up in chunks on one stream, each target-row chunk launches
+    as soon as the source rows it reads (its flanking rows, periodic wrap or
+    wall mirror included) have landed, and its results come back on a third
+    stream while the next chunk computes.  Same arithmetic as the one-shot
+    path (the kernel takes a target-row window, hw_geom2d.trow0/ntrows)."""
+    import torch
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    nsrc = uh.shape[0]
+    tp = flip(parity)
+    shp_u, shp_v = _target_shape2d(grid, parity, m, m), _target_shape2d(grid, parity, m - 1, m - 1)
+    ntx = shp_u[0]
+    srcs = [torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)) for a in (uh, vh)]
+    u = torch.empty(uh.shape, dtype=torch.float64, device=dev)
+    v = torch.empty(vh.shape, dtype=torch.float64, device=dev)
+    ud = torch.empty(shp_u, dtype=torch.float64, device=dev)
+    vd = torch.empty(shp_v, dtype=torch.float64, device=dev)
+    ho_u = torch.empty(shp_u, dtype=torch.float64, pin_memory=True)
+    ho_v = torch.empty(shp_v, dtype=torch.float64, pin_memory=True)
+    comp = torch.cuda.current_stream(dev)
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    s_in.wait_stream(comp)
+    edges = np.linspace(0, nsrc, nchunks + 1).astype(int)
+    arrived = []
+    with torch.cuda.stream(s_in):
+        for a, b in zip(edges[:-1], edges[1:]):
+            u[a:b].copy_(srcs[0][a:b], non_blocking=True)
+            v[a:b].copy_(srcs[1][a:b], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(s_in)
+            arrived.append((a, b, ev))
+    off = 0 if parity == PRIMAL else -1
+    dt = cfg.dt(min(grid.hx, grid.hy))
+    cap = -1 if cfg.stage_cap is None else int(cfg.stage_cap)
+    tedges = np.linspace(0, ntx, nchunks + 1).astype(int)
+    for t0, t1 in zip(tedges[:-1], tedges[1:]):
+        if t1 <= t0:
+            continue
+        need = {min(max(r % nsrc if grid.periodic else r, 0), nsrc - 1) for r in (t0 + off, t1 + off)}
+        need |= set(range(max(t0 + off, 0), min(t1 + off, nsrc - 1) + 1))
+        for a, b, ev in arrived:
+            if any(a <= r < b for r in need):
+                comp.wait_event(ev)
+        g = geom2d(grid, parity, bc, int(t0), int(t1 - t0))
+        L.check(L.lib().hw_diss2d_half_step(C.byref(rows2d(u)), C.byref(rows2d(v)), ptr(ud) + 8 * int(t0) * shp_u[1] *
+                                            (m + 1) ** 2, ptr(vd) + 8 * int(t0) * shp_v[1] * m * m, int(m), C.byref(g),
+                                            dt, grid.hx, grid.hy, cfg.speed, cap, comp.cuda_stream), "half_step_2d")
+        done = torch.cuda.Event()
+        done.record(comp)
+        s_out.wait_event(done)
+        with torch.cuda.stream(s_out):
+            ho_u[t0:t1].copy_(ud[t0:t1], non_blocking=True)
+            ho_v[t0:t1].copy_(vd[t0:t1], non_blocking=True)
+    s_out.synchronize()
+    comp.wait_stream(s_out)
+    return dt, ho_u.numpy(), ho_v.numpy()
+
+
 def half_step_2d(state: FieldPair, cfg: SchemeConfig, bc: BoundarySpec2D) -> FieldPair:
     """Advance 2D (u, v) by dt/2 onto the opposite grid (dissipative.py:215-247)."""
     m = cfg.m
@@ -72,6 +132,13 @@ def half_step_2d(state: FieldPair, cfg: SchemeConfig, bc: BoundarySpec2D) -> Fie
         raise ValueError(f"state carries orders {state.u.orders}, config wants ({m}, {m})")
     for spec in (bc.x, bc.y):
         check_periodicity(spec, grid.periodic)
+    if isinstance(state.u.values, np.ndarray) and isinstance(state.v.values, np.ndarray) and \
+            state.u.values.shape[0] >= 64:
+        require_cuda()
+        dt, hu, hv = _diss2d_host_pipelined(state.u.values, state.v.values, grid, state.parity, m, cfg, bc)
+        t_new = state.time + 0.5 * dt
+        parity = flip(state.parity)
+        return FieldPair(Field2D(grid, parity, t_new, hu), Field2D(grid, parity, t_new, hv))
     st = Staging(state.u.values, state.v.values)
     u = st.to_dev(state.u.values)
     v = st.to_dev(state.v.values)
