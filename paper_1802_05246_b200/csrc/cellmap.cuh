@@ -45,6 +45,19 @@ struct CellMapArgs {
   double gxl, gxh, gyl, gyh;   // Dirichlet data, field 0 only
 };
 
+// Consumer warps per CTA: 12 (three per SM sub-partition, more warps to hide
+// the LDS -> butterfly -> DMMA latency) where that measured faster — the low
+// orders, whose k-steps carry the most non-tensor work per DMMA, and the
+// conservative m = 5 map; 8 elsewhere, where the larger ring and accumulator
+// budget of two warps per sub-partition win (tools/gpu_perf.sh, round 1).
+constexpr int cm_nw(int sch, int m) {
+#ifdef HW_CM_NW
+  return HW_CM_NW;
+#else
+  return (m <= 3 || (sch != kDiss && m == 5) || (sch == kDiss && (m == 6 || m == 7))) ? 12 : 8;
+#endif
+}
+
 template <int M, int SCH>
 struct CMCfg {
   static constexpr int W0 = cm_win(SCH, M, 0), W1 = cm_win(SCH, M, 1);
@@ -58,15 +71,16 @@ struct CMCfg {
   static constexpr int KC = 4 * KSC;               // input slots per chunk
   static constexpr int NCH = (NK + KSC - 1) / KSC; // chunks per tile
   static constexpr int KCP = 20;                   // staged doubles per node (= 4 mod 16: conflict-free)
-  static constexpr int NW = 8;                     // consumer warps
+  static constexpr int NW = cm_nw(SCH, M);         // consumer warps (a multiple of 4)
   static constexpr int NPW = 4;                    // producer warps (one per SM sub-partition)
   static constexpr int NTHREADS = 32 * (NW + NPW);
   static constexpr int TJ = 32;                    // target columns per tile
   static constexpr int DO = O0 + O1;               // output record per cell
   // setmaxnreg split of the 512 registers per lane of each SM sub-partition
-  // (2 consumer + NPW / 4 producer warps)
+  // (NW / 4 consumer + NPW / 4 producer warps)
   static constexpr int PREGS = NPW == 8 ? 56 : 72;
-  static constexpr int CREGS = ((512 - (NPW / 4) * PREGS) / 2) / 8 * 8 > 232 ? 232 : ((512 - (NPW / 4) * PREGS) / 2) / 8 * 8;
+  static constexpr int CREGS0 = ((512 - (NPW / 4) * PREGS) / (NW / 4)) / 8 * 8;
+  static constexpr int CREGS = CREGS0 > 232 ? 232 : CREGS0;
   static constexpr int SMEM_MAX = 227 * 1024;
   // Shared memory for MT M-tiles per consumer warp and an NS-slot ring:
   //   ring slot = the tile's (2 MT + 1) x 33 staged nodes x KCP + 4 k-steps of W
