@@ -283,9 +283,10 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
     return t;
   };
   // M-tile t of consumer warp w in tile `tg`: first target cell and valid count
+  // (the MT M-tiles of a warp are stacked in x: consecutive target rows, same
+  // 8 columns, so neighbouring M-tiles share a row of staged corners)
   auto mtile = [&](const CMTile& tg, int w, int t, int64_t& cell0) {
-    const int mt = w * MT + t;
-    const int trl = mt / (TJ / 8), jl0 = (mt % (TJ / 8)) * 8;
+    const int trl = (w / (TJ / 8)) * MT + t, jl0 = (w % (TJ / 8)) * 8;
     cell0 = (tg.tr0 + trl) * a.nty + tg.j0 + jl0;
     return trl < tg.nvr ? (tg.nvc - jl0 < 8 ? tg.nvc - jl0 : 8) : 0;
   };
@@ -535,18 +536,18 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       constexpr int NKS = decltype(nks_c)::value;
       constexpr bool FIRST = decltype(first_c)::value;
       constexpr bool PREB = C::PREFETCH_B;
-      double raw[2][MT][4];
+      // raw[.][r] = the two y-corners of staged row trl0 + r (row r + 1 of
+      // M-tile r is row 0 of M-tile r + 1: MT + 1 rows feed MT M-tiles)
+      double raw[2][MT + 1][2];
       double bb[PREB ? 2 : 1][NT];
+      const int trl0 = (warp / (TJ / 8)) * MT, tc = (warp % (TJ / 8)) * 8;
+      const double* pbase = cb + (trl0 * (TJ + 1) + tc + (lane >> 2)) * KCP + (lane & 3);
       auto load = [&](const int ks, const int slot) {
 #pragma unroll
-        for (int t = 0; t < MT; ++t) {
-          const int mt = warp * MT + t;
-          const int trl = mt / (TJ / 8), tc = (mt % (TJ / 8)) * 8;
-          const double* p = cb + (trl * (TJ + 1) + tc + (lane >> 2)) * KCP + ks * 4 + (lane & 3);
-          raw[slot][t][0] = p[0];
-          raw[slot][t][1] = p[KCP];
-          raw[slot][t][2] = p[(TJ + 1) * KCP];
-          raw[slot][t][3] = p[(TJ + 2) * KCP];
+        for (int r = 0; r <= MT; ++r) {
+          const double* p = pbase + r * (TJ + 1) * KCP + ks * 4;
+          raw[slot][r][0] = p[0];
+          raw[slot][r][1] = p[KCP];
         }
         if (PREB) {
           const double* wk = wb + ks * NT * 32 + lane;
@@ -567,8 +568,8 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
         for (int t = 0; t < MT; ++t) {
           const double c00 = raw[cur][t][0];
           const double c01 = flip_sign(raw[cur][t][1], my);
-          const double c10 = flip_sign(raw[cur][t][2], mx);
-          const double c11 = flip_sign(raw[cur][t][3], mx ^ my);
+          const double c10 = flip_sign(raw[cur][t + 1][0], mx);
+          const double c11 = flip_sign(raw[cur][t + 1][1], mx ^ my);
           const double ap = c00 + c10, am = c00 - c10, bp = c01 + c11, bm = c01 - c11;
           A[t][0] = ap + bp;  // class (0,0)
           A[t][1] = ap - bp;  // class (0,1)
