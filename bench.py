@@ -190,10 +190,14 @@ def run_reference(args, rank, world):
         return
     m, n = args.m, args.n
     rows = args.ref_rows
-    for _ in range(args.warmup):
+    # bounded: at most 2 warm-up and 10 timed samples of `rows` x n (about 2 s
+    # each at m = 4), whatever --steps / --warmup ask, so the arm ends in well
+    # under a minute; the line reports the sample count it timed
+    n_warm, n_timed = min(args.warmup, 2), min(args.steps, 10)
+    for _ in range(n_warm):
         cpu_sample(m, n, rows)
     tot_t = tot_d = 0.0
-    for _ in range(args.steps):
+    for _ in range(n_timed):
         t, d = cpu_sample(m, n, rows)
         tot_t += t
         tot_d += d
@@ -201,7 +205,8 @@ def run_reference(args, rank, world):
     cores = os.cpu_count()
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / n_timed,
+        "samples_timed": n_timed,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"2D periodic dissipative Hermite m={m}, {n}x{n}, lambda 0.9 (C2)",
                    "m": m, "n": n, "sample_rows": rows},
@@ -218,8 +223,8 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--m", type=int, default=4)
     ap.add_argument("--n", type=int, default=1024)

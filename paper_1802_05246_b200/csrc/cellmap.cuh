@@ -222,7 +222,8 @@ struct CMTile {
 
 // MODE is a profiling knob (tools/cellmap_probe.cu): 0 = the product kernel,
 // 1 = skip the staging copies (compute on whatever the ring holds),
-// 2 = skip the tensor-core work and stores (staging only).
+// 2 = skip the tensor-core work and stores (staging only), 3 = skip the
+// output stores to HBM (staging + tensor cores + slab epilogue).
 template <int M, int SCH, int MODE = 0>
 __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(const __grid_constant__ CellMapArgs a) {
   using C = CMCfg<M, SCH>;
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
         for (int t = 0; t < MT; ++t) {
           int64_t cell0;
           const int nv = mtile(tg, w, t, cell0);
-          if (MODE == 2 || nv == 0) continue;
+          if (MODE == 2 || MODE == 3 || nv == 0) continue;
           double* o0 = a.out0 + cell0 * C::O0;
           const double* s0 = sl + t * NT * 64;
           if (nv == 8) {  // full M-tile: fixed trip counts, loads batched 4 ahead of the stores
@@ -405,7 +406,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
 #pragma unroll
           for (int k = 0; k < NQ; ++k)
             if (q0 + k * QL <= TJ) dst[(r * (TJ + 1) + k * QL) * KCP] = 0.0;
-      } else if (MODE != 1 && MODE != 3 && t.nvr == TR && t.nvc == TJ && t.s_first >= a.f0.row0 &&
+      } else if (MODE != 1 && t.nvr == TR && t.nvc == TJ && t.s_first >= a.f0.row0 &&
                  t.s_first + TR < a.f0.row0 + a.f0.nrows && t.c_first >= 0 && t.c_first + TJ < a.ny) {
         // interior tile: every staged row is a dense segment of the local slab
         const int pf = f1 ? C::P1 : C::P0;
@@ -419,7 +420,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
             if (k < NQ - 1 || q0 + k * QL <= TJ) cm_cp_async8(dst + (r * (TJ + 1) + k * QL) * KCP, src + k * cstep);
           src += rowlen;
         }
-      } else if (MODE != 1 && MODE != 3) {
+      } else if (MODE != 1) {
         const int pf = f1 ? C::P1 : C::P0;
         const int64_t rowlen = a.ny * pf;
         int col[NQ];  // offset of this lane's entry in each staged column (fits 32 bits: ny * P < 2^31)

@@ -34,8 +34,13 @@ float time_variant(const CellMapArgs& a) {
   return best * (per > 0 ? 1.0f : -1.0f);
 }
 
+__global__ void fill(double* p, int64_t n, double scale) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = scale * (double)((i * 2654435761ll) % 1000003 - 500001) / 500001.0;
+}
+
 template <int M, int SCH>
-void probe(int64_t n) {
+void probe(int64_t n, bool zeros) {
   using C = CMCfg<M, SCH>;
   CellMapArgs a;
   memset(&a, 0, sizeof(a));
@@ -51,8 +56,16 @@ void probe(int64_t n) {
   cudaMemset(f0, 0, n * n * C::P0 * 8);
   cudaMemset(f1, 0, n * n * (C::P1 ? C::P1 : 1) * 8);
   cudaMemset(w, 0, C::NK * C::NT * 32 * 8);
+  if (!zeros) {
+    fill<<<1184, 256>>>(f0, n * n * C::P0, 1.0);
+    if (C::P1) fill<<<1184, 256>>>(f1, n * n * C::P1, 1.0);
+    fill<<<64, 256>>>(w, C::NK * C::NT * 32, 0.1);
+  }
   std::vector<int> h(C::NT * 8);
-  for (int i = 0; i < C::NT * 8; ++i) h[i] = i % C::O0;
+  for (int i = 0; i < C::NT * 8; ++i) {  // cover every output of both fields (the drain's inverse map)
+    const int o = i % C::DO;
+    h[i] = o < C::O0 ? o : (1 << 16) | (o - C::O0);
+  }
   cudaMemcpy(oc, h.data(), h.size() * 4, cudaMemcpyHostToDevice);
   cudaMemset(ic, 0, C::NK * 4 * 4);
   a.f0 = {f0, nullptr, nullptr, 0, n};
@@ -68,20 +81,50 @@ void probe(int64_t n) {
   a.ntrows = n;
   a.nty = n;
   a.periodic = 1;
+  fprintf(stderr, "probe m=%d sch=%d zeros=%d: %s\n", M, SCH, (int)zeros, cudaGetErrorString(cudaDeviceSynchronize()));
   const float t0 = time_variant<M, SCH, 0>(a);
+  // 20 back-to-back launches alternating the parity offset (as a time loop does)
+  float tloop = 0.f;
+  {
+    using C = CMCfg<M, SCH>;
+    auto k = cellmap_kernel<M, SCH, 0>;
+    int nsm = 0, per = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, C::NTHREADS, C::SMEM);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    CellMapArgs b = a;
+    cudaEventRecord(e0);
+    for (int r = 0; r < 20; ++r) {
+      b.off = -(r & 1);
+      k<<<nsm * per, C::NTHREADS, C::SMEM>>>(b);
+    }
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&tloop, e0, e1);
+    tloop /= 20.f;
+  }
+  fprintf(stderr, "  t0 %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   const float t1 = time_variant<M, SCH, 1>(a);
   const float t2 = time_variant<M, SCH, 2>(a);
-  printf("{\"m\": %d, \"scheme\": %d, \"n\": %ld, \"full_ms\": %.4f, \"no_staging_ms\": %.4f, \"staging_only_ms\": %.4f, "
+  fprintf(stderr, "  t2 %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
+  const float t3 = time_variant<M, SCH, 3>(a);
+  fprintf(stderr, "  t3 %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
+  printf("{\"zeros\": %d, \"m\": %d, \"scheme\": %d, \"n\": %ld, \"full_ms\": %.4f, \"loop20_alt_parity_ms\": %.4f, \"no_staging_ms\": %.4f, \"staging_only_ms\": %.4f, \"no_hbm_stores_ms\": %.4f, "
          "\"err\": \"%s\"}\n",
-         M, SCH, (long)n, t0, t1, t2, cudaGetErrorString(cudaDeviceSynchronize()));
+         (int)zeros, M, SCH, (long)n, t0, tloop, t1, t2, t3, cudaGetErrorString(cudaDeviceSynchronize()));
   cudaFree(f0); cudaFree(f1); cudaFree(o0); cudaFree(o1); cudaFree(w); cudaFree(oc); cudaFree(ic);
 }
 
 int main(int argc, char** argv) {
   const int64_t n = argc > 1 ? atoll(argv[1]) : 1024;
-  probe<4, kDiss>(n);
-  probe<6, kDiss>(n);
-  probe<8, kDiss>(n);
-  probe<5, kCons>(n);
+  setvbuf(stdout, nullptr, _IOLBF, 0);
+  for (int z = 1; z >= 0; --z) {
+    probe<4, kDiss>(n, z);
+    probe<6, kDiss>(n, z);
+    probe<8, kDiss>(n, z);
+    probe<5, kCons>(n, z);
+  }
   return 0;
 }
