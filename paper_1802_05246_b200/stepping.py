@@ -64,7 +64,7 @@ def diss2d_into(u, v, ud, vd, grid, parity, m, cfg: SchemeConfig, bc: BoundarySp
     return dt
 
 
-def _diss2d_host_pipelined(uh, vh, grid, parity, m, cfg: SchemeConfig, bc: BoundarySpec2D, nchunks: int = 8):
+def _diss2d_host_pipelined(uh, vh, grid, parity, m, cfg: SchemeConfig, bc: BoundarySpec2D, nchunks: int = 16):
     """Host arrays in, host arrays out, with the PCIe traffic overlapped: the
     source rows go up in chunks on one stream, each target-row chunk launches
     as soon as the source rows it reads (its flanking rows, periodic wrap or
@@ -88,16 +88,26 @@ def _diss2d_host_pipelined(uh, vh, grid, parity, m, cfg: SchemeConfig, bc: Bound
     comp = torch.cuda.current_stream(dev)
     s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     s_in.wait_stream(comp)
+    off = 0 if parity == PRIMAL else -1
     edges = np.linspace(0, nsrc, nchunks + 1).astype(int)
+    ranges = list(zip(edges[:-1], edges[1:]))
+    if grid.periodic and off < 0:
+        # the first target rows read the last source row (periodic wrap):
+        # send that row ahead of the chunks so the first launch need not wait
+        # for the whole upload
+        ranges.insert(0, (nsrc - 1, nsrc))
     arrived = []
     with torch.cuda.stream(s_in):
-        for a, b in zip(edges[:-1], edges[1:]):
+        for a, b in ranges:
             u[a:b].copy_(srcs[0][a:b], non_blocking=True)
             v[a:b].copy_(srcs[1][a:b], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(s_in)
             arrived.append((a, b, ev))
-    off = 0 if parity == PRIMAL else -1
+
+    def first_copy(r):  # index of the earliest upload that carries source row r
+        return next(i for i, (a, b, _) in enumerate(arrived) if a <= r < b)
+
     dt = cfg.dt(min(grid.hx, grid.hy))
     cap = -1 if cfg.stage_cap is None else int(cfg.stage_cap)
     tedges = np.linspace(0, ntx, nchunks + 1).astype(int)
@@ -106,9 +116,9 @@ def _diss2d_host_pipelined(uh, vh, grid, parity, m, cfg: SchemeConfig, bc: Bound
             continue
         need = {min(max(r % nsrc if grid.periodic else r, 0), nsrc - 1) for r in (t0 + off, t1 + off)}
         need |= set(range(max(t0 + off, 0), min(t1 + off, nsrc - 1) + 1))
-        for a, b, ev in arrived:
-            if any(a <= r < b for r in need):
-                comp.wait_event(ev)
+        # uploads complete in issue order (one stream): waiting on the latest
+        # one this chunk needs covers the rest
+        comp.wait_event(arrived[max(first_copy(r) for r in need)][2])
         g = geom2d(grid, parity, bc, int(t0), int(t1 - t0))
         L.check(L.lib().hw_diss2d_half_step(C.byref(rows2d(u)), C.byref(rows2d(v)), ptr(ud) + 8 * int(t0) * shp_u[1] *
                                             (m + 1) ** 2, ptr(vd) + 8 * int(t0) * shp_v[1] * m * m, int(m), C.byref(g),
