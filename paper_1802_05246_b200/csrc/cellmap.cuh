@@ -45,19 +45,6 @@ struct CellMapArgs {
   double gxl, gxh, gyl, gyh;   // Dirichlet data, field 0 only
 };
 
-// Consumer warps per CTA: 12 (three per SM sub-partition, more warps to hide
-// the LDS -> butterfly -> DMMA latency) where that measured faster — the low
-// orders, whose k-steps carry the most non-tensor work per DMMA, and the
-// conservative m = 5 map; 8 elsewhere, where the larger ring and accumulator
-// budget of two warps per sub-partition win (tools/gpu_perf.sh, round 1).
-constexpr int cm_nw(int sch, int m) {
-#ifdef HW_CM_NW
-  return HW_CM_NW;
-#else
-  return (m <= 3 || (sch != kDiss && m == 5) || (sch == kDiss && (m == 6 || m == 7))) ? 12 : 8;
-#endif
-}
-
 template <int M, int SCH>
 struct CMCfg {
   static constexpr int W0 = cm_win(SCH, M, 0), W1 = cm_win(SCH, M, 1);
@@ -67,7 +54,7 @@ struct CMCfg {
   static constexpr int O1 = cm_wout(SCH, M, 1) * cm_wout(SCH, M, 1);
   static constexpr int NK = cm_nk(SCH, M), NT = cm_nt(SCH, M);
   static constexpr int B1 = cm_ntbase(SCH, M, 1), B2 = cm_ntbase(SCH, M, 2), B3 = cm_ntbase(SCH, M, 3);
-  static constexpr int KSC = 4;                    // k-steps per chunk
+  static constexpr int KSC = cm_ksc();             // k-steps per chunk
   static constexpr int KC = 4 * KSC;               // input slots per chunk
   static constexpr int NCH = (NK + KSC - 1) / KSC; // chunks per tile
   static constexpr int KCP = 20;                   // staged doubles per node (= 4 mod 16: conflict-free)
@@ -92,6 +79,14 @@ struct CMCfg {
     return NW * (mt * NT * 64 + (SCH == kCons ? mt * 8 * O0 : 0)) * 8 + (8 * DO + 8 * NT) * 4 + (8 + 2 * NW) * 8 + 64;
   }
   static constexpr bool fits(int mt, int ns) { return ns * sbuf(mt) * 8 + tail(mt) <= SMEM_MAX; }
+  // Ring depth: 4 slots only where they leave >= 56 KB of the SM's 256 KB
+  // L1/shared array to L1, else 3 where they fit at all.  A 4-slot ring that
+  // eats into L1 measured slower than 3 slots (m = 5: 218 KB 0.44 ms vs 183 KB
+  // 0.39 ms; m = 6 and conservative m = 8 likewise: the cp.async staging
+  // needs the L1 lines), while 2 slots starve the consumers (m = 7: 3 slots at
+  // 215 KB beat 2 at 178 KB by 8%).
+  static constexpr int SMEM_SOFT = 200 * 1024;
+  static constexpr bool fits_soft(int mt, int ns) { return ns * sbuf(mt) * 8 + tail(mt) <= SMEM_SOFT; }
   // 8-cell M-tiles per consumer warp.  Each staged W fragment feeds MT DMMAs
   // and each corner load feeds NT, so shared-memory traffic per DMMA falls as
   // (4 MT + NT) / (MT NT): take MT = 2 where its accumulators (2 MT NT
@@ -106,7 +101,11 @@ struct CMCfg {
   static constexpr int SLAB = MT * NT * 64;
   static constexpr int PSLAB = SCH == kCons ? MT * 8 * O0 : 0;
   static constexpr int TAIL = tail(MT);
-  static constexpr int NS = fits(MT, 4) ? 4 : (fits(MT, 3) ? 3 : 2);  // ring depth
+#ifdef HW_CM_NS
+  static constexpr int NS = fits(MT, HW_CM_NS) ? HW_CM_NS : (fits(MT, 3) ? 3 : 2);
+#else
+  static constexpr int NS = fits_soft(MT, 4) ? 4 : (fits(MT, 3) ? 3 : 2);
+#endif
   static constexpr int EPI0 = NS * SBUF;           // double offset of the slabs
   static constexpr int SMEM = NS * SBUF * 8 + TAIL;
   static constexpr bool PREFETCH_B = NT <= 9;      // W fragments double-buffered in registers too

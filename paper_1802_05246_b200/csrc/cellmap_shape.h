@@ -45,4 +45,20 @@ constexpr int cm_nk(int sch, int m) {
   return (cm_k0(sch, m) + (cm_win(sch, m, 1) * cm_win(sch, m, 1) + 3) / 4 * 4) / 4;
 }
 
+// The kernel's staging unit: k-steps per ring chunk.
+constexpr int cm_ksc() { return 4; }
+
+// Consumer warps per CTA: 12 (three per SM sub-partition, more warps to hide
+// the LDS -> butterfly -> DMMA latency) where that measured faster — the low
+// orders, whose k-steps carry the most non-tensor work per DMMA, and the
+// conservative m = 5 map; 8 elsewhere, where the larger ring and accumulator
+// budget of two warps per sub-partition win (tools/gpu_perf.sh, round 1).
+constexpr int cm_nw(int sch, int m) {
+#ifdef HW_CM_NW
+  return HW_CM_NW;
+#else
+  return (m <= 3 || (sch != 0 && m == 5) || (sch == 0 && (m == 6 || m == 7))) ? 12 : 8;
+#endif
+}
+
 }  // namespace hw

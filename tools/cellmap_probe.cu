@@ -120,8 +120,9 @@ void probe(int64_t n, bool zeros) {
 int main(int argc, char** argv) {
   const int64_t n = argc > 1 ? atoll(argv[1]) : 1024;
   setvbuf(stdout, nullptr, _IOLBF, 0);
-  for (int z = 1; z >= 0; --z) {
+  for (int z = 1; z >= 1; --z) {
     probe<4, kDiss>(n, z);
+    probe<5, kDiss>(n, z);
     probe<6, kDiss>(n, z);
     probe<8, kDiss>(n, z);
     probe<5, kCons>(n, z);
