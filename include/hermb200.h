@@ -163,6 +163,20 @@ int hw_l2err2d(const hw_rows2d* src, int mx, int my, const hw_geom2d* geom,
                double* out_host, void* stream);
 
 /*
+ * Squared 2D seminorm sum_cells int int (d^dx/dx^dx d^dy/dy^dy I u)^2 dx dy
+ * of the tensor interpolant I = I_{mx,my} over the target cells of the
+ * field's own corner gather (the cells of hw_l2err2d), by npts^2-point Gauss
+ * quadrature (exact when 2 npts - 1 >= 2 (2 max(mx,my) + 1)).  The building
+ * block of the defined 2D energy (norms.py dissipative_energy_2d; no
+ * reference counterpart: diagnostics.py:220-234 is 1D only).  Result ->
+ * *out_host after a stream synchronisation.
+ */
+int hw_seminorm2d(const hw_rows2d* src, int mx, int my, const hw_geom2d* geom,
+                  double hx, double hy, int dx, int dy, int npts,
+                  const double* gauss_x, const double* gauss_w,
+                  double* out_host, void* stream);
+
+/*
  * diagnostics.py:66-115 per-piece 1D L2 errors.  For each target piece t the
  * caller supplies the clipped Gauss abscissae in the piece's scaled variable
  * (xi[t][p]), the weights times half-width (w[t][p]) and the exact values

@@ -455,6 +455,39 @@ def dissipative_energy_1d(u, v, parity, n, periodic, h, speed, bc=PERIODIC_BC):
         seminorm_sq_1d(v, parity, n, periodic, h, m, bc)
 
 
+# ----------------------------------------------------------------- energy (2D, defined here)
+
+def _monomial_gram(n):
+    """G[a][b] = int_{-1/2}^{1/2} xi^(a+b) dxi, exactly."""
+    k = np.add.outer(np.arange(n), np.arange(n))
+    return np.where(k % 2 == 0, 2.0 * 0.5 ** (k + 1) / (k + 1), 0.0)
+
+
+def seminorm_sq_2d(values, parity, hx, hy, dx, dy):
+    """sum_cells int int (d_x^dx d_y^dy I u)^2 of the tensor interpolant on a
+    periodic grid: cell coefficients from corner_data + interp_2d, derivative
+    taken on the monomial coefficients, the square integrated in closed form
+    (a Gram matrix of monomials — independent of the device's Gauss rule).
+    No reference counterpart (the reference energies are 1D only)."""
+    c = interp_2d(corner_data(values, parity, True, PERIODIC_BC, PERIODIC_BC))
+    nxc, nyc = c.shape[-2] - dx, c.shape[-1] - dy
+    if nxc <= 0 or nyc <= 0:
+        return 0.0
+    fx = np.array([math.factorial(a + dx) / math.factorial(a) for a in range(nxc)]) / hx**dx
+    fy = np.array([math.factorial(b + dy) / math.factorial(b) for b in range(nyc)]) / hy**dy
+    d = c[..., dx:, dy:] * fx[:, None] * fy[None, :]
+    return float(hx * hy * np.einsum("ijab,ac,ijcd,bd->", d, _monomial_gram(nxc), d, _monomial_gram(nyc)))
+
+
+def dissipative_energy_2d(u, v, parity, hx, hy, speed):
+    """c^2 (|d_x^{m+1} I u|^2 + |d_y^{m+1} I u|^2) + |d_x^m I v|^2 + |d_y^m I v|^2
+    (paper_1802_05246_b200.norms.dissipative_energy_2d's definition)."""
+    m = u.shape[-1] - 1
+    eu = seminorm_sq_2d(u, parity, hx, hy, m + 1, 0) + seminorm_sq_2d(u, parity, hx, hy, 0, m + 1)
+    ev = seminorm_sq_2d(v, parity, hx, hy, m, 0) + seminorm_sq_2d(v, parity, hx, hy, 0, m)
+    return speed * speed * eu + ev
+
+
 def conservative_energy_1d(cur, prev, parity_cur, n, h, delta):
     """diagnostics.py:190-226 on a periodic grid, restated per union piece.
 

@@ -17,6 +17,7 @@ from .norms import (
     conservative_energy,
     default_npts,
     dissipative_energy,
+    dissipative_energy_2d,
     fit_rate,
     gauss_rule,
     l2_error_field,
@@ -42,7 +43,7 @@ __all__ = [
     "DUAL", "PRIMAL", "Field1D", "Field2D", "FieldPair", "Grid1D", "Grid2D", "TwoLevelState", "flip",
     "planewave_on_grid", "standing_wave_on_grid",
     "ErrorReport", "PlaneWave2D", "StandingWave2D", "default_npts", "fit_rate", "gauss_rule",
-    "dissipative_energy", "conservative_energy",
+    "dissipative_energy", "dissipative_energy_2d", "conservative_energy",
     "l2_error_field", "l2_error_field_2d", "l2_errors_pair",
     "NumericalError", "advance_2d", "advance_conservative", "bootstrap_first_half",
     "full_step_conservative", "half_step_1d", "half_step_2d", "interp_matrix", "require_finite",

@@ -1,5 +1,6 @@
 // extern "C" boundary (include/hermb200.h): argument checking, constant-table
 // construction and kernel dispatch.  Never throws across the ABI.
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <list>
@@ -463,6 +464,89 @@ static double reduce_partials(double* part, int64_t n, cudaStream_t st) {
   return h;
 }
 
+// Shared by hw_l2err2d and hw_seminorm2d: the tensor interpolant of every
+// target cell evaluated at the npts^2 Gauss points, d-th derivative along each
+// axis (d = 0: the values), reduced to sum_cells sum_pq w_p w_q (val - exact)^2.
+static double cell_quadrature_2d(const hw_rows2d* src, int mx, int my, const hw_geom2d* geom, double x_left,
+                                 double y_left, double hx, double hy, int dx, int dy, int npts,
+                                 const double* gauss_x, const double* gauss_w, int exact_kind, const double* exact,
+                                 const double* params, cudaStream_t st) {
+  const Geo g = check_geom(geom);
+  // Ex[p][e] = sum_a d^dx/dx^dx (xg_p/2)^a M[a][e]   (diagnostics.py:128-130 at dx = 0);
+  // the interpolant is a polynomial in xi = (x - xc) / h, so each derivative brings 1/h
+  std::vector<double> gx(npts), gw(npts);
+  cuda_check(cudaMemcpy(gx.data(), gauss_x, npts * sizeof(double), cudaMemcpyDefault), "copy gauss x");
+  cuda_check(cudaMemcpy(gw.data(), gauss_w, npts * sizeof(double), cudaMemcpyDefault), "copy gauss w");
+  auto emat = [&](int mu, int d, double h) {
+    const std::vector<double> M = hermite_matrix(mu);
+    const int n = 2 * mu + 2;
+    std::vector<double> e((size_t)npts * n, 0.0);
+    for (int p = 0; p < npts; ++p) {
+      const double xi = 0.5 * gx[p];
+      for (int c = 0; c < n; ++c) {
+        double s = 0.0, pw = 1.0;
+        for (int a2 = d; a2 < n; ++a2) {
+          double fall = 1.0;  // a2! / (a2 - d)!
+          for (int k = 0; k < d; ++k) fall *= (double)(a2 - k);
+          s += fall * pw * M[(size_t)a2 * n + c];
+          pw *= xi;
+        }
+        e[(size_t)p * n + c] = d ? s * std::pow(h, -(double)d) : s;
+      }
+    }
+    return e;
+  };
+  const std::vector<double> ex = emat(mx, dx, hx), ey = emat(my, dy, hy);
+  const int64_t ncell = g.ntx * g.nty;
+  const int64_t nblk = (ncell + kRedThreads - 1) / kRedThreads;
+  DevBuf dex, dey, dgx, dgw, dpart;
+  cuda_check(cudaMalloc(&dex.p, ex.size() * 8), "cudaMalloc");
+  cuda_check(cudaMalloc(&dey.p, ey.size() * 8), "cudaMalloc");
+  cuda_check(cudaMalloc(&dgx.p, npts * 8), "cudaMalloc");
+  cuda_check(cudaMalloc(&dgw.p, npts * 8), "cudaMalloc");
+  cuda_check(cudaMalloc(&dpart.p, nblk * 8), "cudaMalloc");
+  cuda_check(cudaMemcpy(dex.p, ex.data(), ex.size() * 8, cudaMemcpyHostToDevice), "cudaMemcpy");
+  cuda_check(cudaMemcpy(dey.p, ey.data(), ey.size() * 8, cudaMemcpyHostToDevice), "cudaMemcpy");
+  cuda_check(cudaMemcpy(dgx.p, gx.data(), npts * 8, cudaMemcpyHostToDevice), "cudaMemcpy");
+  cuda_check(cudaMemcpy(dgw.p, gw.data(), npts * 8, cudaMemcpyHostToDevice), "cudaMemcpy");
+  L2Err2DArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.f = to_rows(src);
+  a.nx = g.nx;
+  a.ny = g.ny;
+  a.ntx = g.ntx;
+  a.nty = g.nty;
+  a.off = g.off;
+  a.periodic = g.periodic;
+  a.kxl = g.periodic ? 0 : geom->bcx.left_kind;
+  a.kxh = g.periodic ? 0 : geom->bcx.right_kind;
+  a.kyl = g.periodic ? 0 : geom->bcy.left_kind;
+  a.kyh = g.periodic ? 0 : geom->bcy.right_kind;
+  a.gxl = geom->bcx.left_value;
+  a.gxh = geom->bcx.right_value;
+  a.gyl = geom->bcy.left_value;
+  a.gyh = geom->bcy.right_value;
+  a.mx = mx;
+  a.my = my;
+  a.npts = npts;
+  a.ex = dex.p;
+  a.ey = dey.p;
+  a.gw = dgw.p;
+  a.gx = dgx.p;
+  a.exact_kind = exact_kind;
+  a.exact = exact;
+  for (int q = 0; q < 4; ++q) a.prm[q] = params ? params[q] : 0.0;
+  a.x0 = x_left;
+  a.y0 = y_left;
+  a.hx = hx;
+  a.hy = hy;
+  a.coff = geom->parity_src == HW_PRIMAL ? 0.5 : 0.0;  // targets live on the flipped parity
+  a.part = dpart.p;
+  l2err2d_kernel<<<(unsigned)nblk, kRedThreads, 0, st>>>(a);
+  cuda_check(cudaGetLastError(), "l2err2d launch");
+  return reduce_partials(dpart.p, nblk, st);
+}
+
 int hw_l2err2d(const hw_rows2d* src, int mx, int my, const hw_geom2d* geom, double x_left, double y_left,
                double hx, double hy, int npts, const double* gauss_x, const double* gauss_w, int exact_kind,
                const double* exact, const double* params, double* out_host, void* stream) {
@@ -472,78 +556,21 @@ int hw_l2err2d(const hw_rows2d* src, int mx, int my, const hw_geom2d* geom, doub
     HW_CHECK(npts >= 1 && npts <= 64, "npts out of range");
     HW_CHECK(exact_kind >= 0 && exact_kind <= 2, "unknown exact kind");
     HW_CHECK(exact_kind != 0 || exact, "null exact array");
-    const Geo g = check_geom(geom);
-    cudaStream_t st = (cudaStream_t)stream;
-    // Ex[p][e] = sum_a (xg_p/2)^a M[a][e]   (diagnostics.py:128-130)
-    std::vector<double> gx(npts), gw(npts);
-    cuda_check(cudaMemcpy(gx.data(), gauss_x, npts * sizeof(double), cudaMemcpyDefault), "copy gauss x");
-    cuda_check(cudaMemcpy(gw.data(), gauss_w, npts * sizeof(double), cudaMemcpyDefault), "copy gauss w");
-    auto emat = [&](int mu) {
-      const std::vector<double> M = hermite_matrix(mu);
-      const int n = 2 * mu + 2;
-      std::vector<double> e((size_t)npts * n, 0.0);
-      for (int p = 0; p < npts; ++p) {
-        const double xi = 0.5 * gx[p];
-        for (int c = 0; c < n; ++c) {
-          double s = 0.0, pw = 1.0;
-          for (int a2 = 0; a2 < n; ++a2) {
-            s += pw * M[(size_t)a2 * n + c];
-            pw *= xi;
-          }
-          e[(size_t)p * n + c] = s;
-        }
-      }
-      return e;
-    };
-    const std::vector<double> ex = emat(mx), ey = emat(my);
-    const int64_t ncell = g.ntx * g.nty;
-    const int64_t nblk = (ncell + kRedThreads - 1) / kRedThreads;
-    DevBuf dex, dey, dgx, dgw, dpart;
-    cuda_check(cudaMalloc(&dex.p, ex.size() * 8), "cudaMalloc");
-    cuda_check(cudaMalloc(&dey.p, ey.size() * 8), "cudaMalloc");
-    cuda_check(cudaMalloc(&dgx.p, npts * 8), "cudaMalloc");
-    cuda_check(cudaMalloc(&dgw.p, npts * 8), "cudaMalloc");
-    cuda_check(cudaMalloc(&dpart.p, nblk * 8), "cudaMalloc");
-    cuda_check(cudaMemcpy(dex.p, ex.data(), ex.size() * 8, cudaMemcpyHostToDevice), "cudaMemcpy");
-    cuda_check(cudaMemcpy(dey.p, ey.data(), ey.size() * 8, cudaMemcpyHostToDevice), "cudaMemcpy");
-    cuda_check(cudaMemcpy(dgx.p, gx.data(), npts * 8, cudaMemcpyHostToDevice), "cudaMemcpy");
-    cuda_check(cudaMemcpy(dgw.p, gw.data(), npts * 8, cudaMemcpyHostToDevice), "cudaMemcpy");
-    L2Err2DArgs a;
-    std::memset(&a, 0, sizeof(a));
-    a.f = to_rows(src);
-    a.nx = g.nx;
-    a.ny = g.ny;
-    a.ntx = g.ntx;
-    a.nty = g.nty;
-    a.off = g.off;
-    a.periodic = g.periodic;
-    a.kxl = g.periodic ? 0 : geom->bcx.left_kind;
-    a.kxh = g.periodic ? 0 : geom->bcx.right_kind;
-    a.kyl = g.periodic ? 0 : geom->bcy.left_kind;
-    a.kyh = g.periodic ? 0 : geom->bcy.right_kind;
-    a.gxl = geom->bcx.left_value;
-    a.gxh = geom->bcx.right_value;
-    a.gyl = geom->bcy.left_value;
-    a.gyh = geom->bcy.right_value;
-    a.mx = mx;
-    a.my = my;
-    a.npts = npts;
-    a.ex = dex.p;
-    a.ey = dey.p;
-    a.gw = dgw.p;
-    a.gx = dgx.p;
-    a.exact_kind = exact_kind;
-    a.exact = exact;
-    for (int q = 0; q < 4; ++q) a.prm[q] = params ? params[q] : 0.0;
-    a.x0 = x_left;
-    a.y0 = y_left;
-    a.hx = hx;
-    a.hy = hy;
-    a.coff = geom->parity_src == HW_PRIMAL ? 0.5 : 0.0;  // targets live on the flipped parity
-    a.part = dpart.p;
-    l2err2d_kernel<<<(unsigned)nblk, kRedThreads, 0, st>>>(a);
-    cuda_check(cudaGetLastError(), "l2err2d launch");
-    const double s = reduce_partials(dpart.p, nblk, st);
+    const double s = cell_quadrature_2d(src, mx, my, geom, x_left, y_left, hx, hy, 0, 0, npts, gauss_x, gauss_w,
+                                        exact_kind, exact, params, (cudaStream_t)stream);
+    *out_host = s * (0.25 * hx * hy);
+  });
+}
+
+int hw_seminorm2d(const hw_rows2d* src, int mx, int my, const hw_geom2d* geom, double hx, double hy, int dx, int dy,
+                  int npts, const double* gauss_x, const double* gauss_w, double* out_host, void* stream) {
+  return guard([&] {
+    HW_CHECK(src && src->base && gauss_x && gauss_w && out_host, "null pointer");
+    HW_CHECK(mx >= 0 && my >= 0 && mx <= kMaxOrder && my <= kMaxOrder, "orders out of range");
+    HW_CHECK(dx >= 0 && dy >= 0 && dx <= 2 * mx + 1 && dy <= 2 * my + 1, "derivative orders out of range");
+    HW_CHECK(npts >= 1 && npts <= 64, "npts out of range");
+    const double s = cell_quadrature_2d(src, mx, my, geom, 0.0, 0.0, hx, hy, dx, dy, npts, gauss_x, gauss_w, 3,
+                                        nullptr, nullptr, (cudaStream_t)stream);
     *out_host = s * (0.25 * hx * hy);
   });
 }

@@ -54,6 +54,8 @@ __device__ inline double exact_builtin(int kind, const double* prm, double x, do
 }
 
 // diagnostics.py:118-135 l2_error_field_2d: one thread per target cell.
+// exact_kind 3 (no exact solution) with derivative evaluation matrices Ex/Ey
+// gives the squared seminorm sum of the 2D energy (hw_seminorm2d).
 __global__ void l2err2d_kernel(L2Err2DArgs a) {
   __shared__ double sh[kRedThreads];
   const int64_t ncell = a.ntx * a.nty;
@@ -92,6 +94,8 @@ __global__ void l2err2d_kernel(L2Err2DArgs a) {
         double ex;
         if (a.exact_kind == 0) {
           ex = a.exact[((ti * a.nty + tj) * a.npts + p) * a.npts + q];
+        } else if (a.exact_kind == 3) {  // seminorms: the derivative interpolant alone
+          ex = 0.0;
         } else {
           const double xp = cx + 0.5 * a.hx * a.gx[p];
           ex = exact_builtin(a.exact_kind, a.prm, xp, yq);

@@ -206,6 +206,45 @@ def dissipative_energy(state: FieldPair, speed: float, bc: BoundarySpec) -> floa
     return (_seminorm_sq(state.u, bc, m + 1, speed * speed, st) + _seminorm_sq(state.v, bc, m, 1.0, st))
 
 
+def _seminorm_sq_2d(field: Field2D, dx: int, dy: int, npts: int, st) -> float:
+    grid = field.grid
+    mx, my = field.orders
+    g = geom2d(grid, field.parity, BoundarySpec2D())
+    xg, wg = gauss_rule(npts)
+    gx = np.ascontiguousarray(xg, dtype=np.float64)
+    gw = np.ascontiguousarray(wg, dtype=np.float64)
+    f = st.to_dev(field.values)
+    out = C.c_double(0.0)
+    L.check(L.lib().hw_seminorm2d(C.byref(rows2d(f)), int(mx), int(my), C.byref(g), grid.hx, grid.hy, int(dx),
+                                  int(dy), int(npts), gx.ctypes.data_as(C.c_void_p), gw.ctypes.data_as(C.c_void_p),
+                                  C.byref(out), st.stream), "dissipative_energy_2d")
+    return out.value
+
+
+def dissipative_energy_2d(state: FieldPair, speed: float) -> float:
+    """A defined 2D energy of a dissipative state (the
+    reference has none — diagnostics.py:220-234 and the paper's proof are 1D):
+
+        E = c^2 (|d_x^{m+1} I u|^2 + |d_y^{m+1} I u|^2) + |d_x^m I v|^2 + |d_y^m I v|^2,
+
+    I = the tensor Hermite interpolants I_{m,m} u and I_{m-1,m-1} v on every
+    cell of the field's periodic grid, |.|^2 the L2 norm over the domain,
+    integrated exactly (Gauss, 2m + 2 points per axis).  On y-independent data
+    it is L_y times the 1D dissipative_energy (diagnostics.py:229-234) of the
+    x-profile — the reduction the tests pin it by."""
+    grid = state.u.grid
+    if not grid.periodic:
+        raise ValueError("the 2D energy is defined on periodic grids")
+    m = state.u.orders[0]
+    if state.u.orders != (m, m) or state.v.orders != (m - 1, m - 1):
+        raise ValueError(f"pair carries orders {state.u.orders} / {state.v.orders}, want (m, m) / (m-1, m-1)")
+    npts = 2 * m + 2
+    st = Staging(state.u.values, state.v.values)
+    eu = _seminorm_sq_2d(state.u, m + 1, 0, npts, st) + _seminorm_sq_2d(state.u, 0, m + 1, npts, st)
+    ev = _seminorm_sq_2d(state.v, m, 0, npts, st) + _seminorm_sq_2d(state.v, 0, m, npts, st)
+    return speed * speed * eu + ev
+
+
 def conservative_energy(current: Field1D, previous: Field1D, speed: float, dt: float, bc: BoundarySpec) -> float:
     """E(t_n) = |P+|^2_{m+1} + |P-|^2_{m+1} of a two-level state (diagnostics.py:190-226).
 

@@ -100,3 +100,92 @@ def test_device_energy_errors():
         hb.conservative_energy(f, g, 1.0, 2.0 * gp.h, hb.BoundarySpec())
     assert hb.dissipative_energy(hb.FieldPair(f, hb.Field1D(gp, hb.PRIMAL, 0.0, np.zeros((6, 2)))), 2.0,
                                  hb.BoundarySpec()) == 0.0
+
+
+# ------------------------------------------------------------ the defined 2D energy
+# No reference counterpart exists (the reference's energies are 1D).  It is
+# pinned by (i) reduction to the REFERENCE's 1D dissipative energy on
+# y-independent data, (ii) an oracle that integrates the interpolants in
+# closed form (monomial Gram matrices) rather than by the device's Gauss rule.
+PERIODIC_DISS = [c for c in DISS if c[3]]
+LY, NY = 0.7, 5
+
+
+def _extend_y(u1, v1):
+    """y-independent 2D fields whose x-profile is the 1D pair (l = 0 blocks)."""
+    n, m = u1.shape[0], u1.shape[1] - 1
+    u2 = np.zeros((n, NY, m + 1, m + 1))
+    v2 = np.zeros((n, NY, m, m))
+    u2[:, :, :, 0] = u1[:, None, :]
+    v2[:, :, :, 0] = v1[:, None, :]
+    return u2, v2
+
+
+@pytest.mark.parametrize("case", PERIODIC_DISS, ids=[c[0] for c in PERIODIC_DISS])
+def test_oracle_energy_2d_reduces_to_reference_1d(gold, case):
+    name, m, n, per, par, bcs, speed = case
+    u2, v2 = _extend_y(gold[f"ed/{name}/u"], gold[f"ed/{name}/v"])
+    e2 = O.dissipative_energy_2d(u2, v2, par, _h(n), LY / NY, speed)
+    assert e2 == pytest.approx(LY * float(gold[f"ed/{name}/e"]), rel=1e-13)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", PERIODIC_DISS, ids=[c[0] for c in PERIODIC_DISS])
+def test_device_energy_2d_reduces_to_reference_1d(gold, case):
+    import paper_1802_05246_b200 as hb
+
+    name, m, n, per, par, bcs, speed = case
+    u2, v2 = _extend_y(gold[f"ed/{name}/u"], gold[f"ed/{name}/v"])
+    grid = hb.Grid2D(X1D[0], X1D[1], 0.0, LY, n, NY, True)
+    pair = hb.FieldPair(hb.Field2D(grid, par, 0.0, u2), hb.Field2D(grid, par, 0.0, v2))
+    assert hb.dissipative_energy_2d(pair, speed) == pytest.approx(LY * float(gold[f"ed/{name}/e"]), rel=1e-12)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,par", [(1, O.PRIMAL), (2, O.DUAL), (4, O.PRIMAL), (6, O.DUAL), (8, O.PRIMAL)])
+def test_device_energy_2d_matches_closed_form_oracle(m, par):
+    import paper_1802_05246_b200 as hb
+
+    rng = np.random.default_rng(300 + m)
+    nx, ny = 9, 7
+    grid = hb.Grid2D(-0.2, 0.9, 0.1, 1.3, nx, ny, True)
+    u = rng.standard_normal((nx, ny, m + 1, m + 1))
+    v = rng.standard_normal((nx, ny, m, m))
+    pair = hb.FieldPair(hb.Field2D(grid, par, 0.0, u), hb.Field2D(grid, par, 0.0, v))
+    want = O.dissipative_energy_2d(u, v, par, grid.hx, grid.hy, 1.3)
+    # Gauss vs closed form: the rounding of a sum of O(cells * npts^2) squares
+    # of interpolants amplified by cond(M_mu) (SURVEY App. A.3)
+    assert hb.dissipative_energy_2d(pair, 1.3) == pytest.approx(want, rel={8: 1e-9, 6: 1e-11}.get(m, 1e-12))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m", [2, 4])
+def test_device_energy_2d_does_not_grow_under_the_dissipative_step(m):
+    """Observed (not proven) analogue of test_dissipative.py:196-230: the
+    defined 2D energy of random data is non-increasing over half steps."""
+    import paper_1802_05246_b200 as hb
+
+    rng = np.random.default_rng(20 + m)
+    n = 16
+    grid = hb.Grid2D(0.0, 1.0, 0.0, 1.0, n, n, True)
+    cfg = hb.SchemeConfig(m=m, lam=0.9)
+    p = hb.FieldPair(hb.Field2D(grid, hb.PRIMAL, 0.0, rng.standard_normal((n, n, m + 1, m + 1))),
+                     hb.Field2D(grid, hb.PRIMAL, 0.0, rng.standard_normal((n, n, m, m))))
+    es = [hb.dissipative_energy_2d(p, 1.0)]
+    for _ in range(6):
+        p = hb.half_step_2d(p, cfg, hb.BoundarySpec2D())
+        es.append(hb.dissipative_energy_2d(p, 1.0))
+    assert all(b <= a * (1 + 1e-12) for a, b in zip(es, es[1:]))
+    assert es[-1] < 0.5 * es[0]
+
+
+@pytest.mark.gpu
+def test_device_energy_2d_errors():
+    import paper_1802_05246_b200 as hb
+
+    m = 2
+    grid = hb.Grid2D(0.0, 1.0, 0.0, 1.0, 4, 4, False)
+    u = np.zeros((5, 5, m + 1, m + 1))
+    v = np.zeros((5, 5, m, m))
+    with pytest.raises(ValueError, match="periodic"):
+        hb.dissipative_energy_2d(hb.FieldPair(hb.Field2D(grid, hb.PRIMAL, 0.0, u), hb.Field2D(grid, hb.PRIMAL, 0.0, v)), 1.0)
