@@ -121,11 +121,17 @@ int main(int argc, char** argv) {
   const int64_t n = argc > 1 ? atoll(argv[1]) : 1024;
   setvbuf(stdout, nullptr, _IOLBF, 0);
   for (int z = 1; z >= 1; --z) {
+    probe<2, kDiss>(n, z);
+    probe<3, kDiss>(n, z);
     probe<4, kDiss>(n, z);
     probe<5, kDiss>(n, z);
     probe<6, kDiss>(n, z);
+    probe<7, kDiss>(n, z);
     probe<8, kDiss>(n, z);
+    probe<3, kCons>(n, z);
+    probe<4, kCons>(n, z);
     probe<5, kCons>(n, z);
+    probe<8, kCons>(n, z);
   }
   return 0;
 }
