@@ -6,20 +6,21 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O2 --expt-relaxed-constexpr
 CXXFLAGS := -O2 -fPIC -std=c++17
 SRC := paper_1802_05246_b200/csrc
-LIB := paper_1802_05246_b200/libhermb200.so
+LIB ?= paper_1802_05246_b200/libhermb200.so
+BUILD ?= build
 HDRS := $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.h) include/hermb200.h
-KERN := $(patsubst $(SRC)/%.cu,build/%.o,$(wildcard $(SRC)/kern_m*.cu))
-OBJ := build/capi.o build/tables.o build/cellmap.o $(KERN)
+KERN := $(patsubst $(SRC)/%.cu,$(BUILD)/%.o,$(wildcard $(SRC)/kern_m*.cu))
+OBJ := $(BUILD)/capi.o $(BUILD)/tables.o $(BUILD)/cellmap.o $(KERN)
 
 all: $(LIB) tools/fp64_peak
 
-build/%.o: $(SRC)/%.cu $(HDRS)
-	@mkdir -p build
-	$(NVCC) $(NVFLAGS) $(PTXAS) -c $< -o $@
+$(BUILD)/%.o: $(SRC)/%.cu $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) $(PTXAS) $(EXTRA) -c $< -o $@
 
-build/%.o: $(SRC)/%.cpp $(HDRS)
-	@mkdir -p build
-	g++ $(CXXFLAGS) -c $< -o $@
+$(BUILD)/%.o: $(SRC)/%.cpp $(HDRS)
+	@mkdir -p $(BUILD)
+	g++ $(CXXFLAGS) $(EXTRA) -c $< -o $@
 
 $(LIB): $(OBJ)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lcudart

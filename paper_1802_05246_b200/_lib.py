@@ -12,7 +12,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhermb200.so")
+# HERMB200_LIB: an alternative build of the same library (A/B timing of kernel variants, tools/build_variant.sh)
+LIB_PATH = os.environ.get("HERMB200_LIB") or os.path.join(_HERE, "libhermb200.so")
 
 HW_PERIODIC, HW_DIRICHLET0, HW_NEUMANN0 = 0, 1, 2
 HW_PRIMAL, HW_DUAL = 0, 1

@@ -74,9 +74,15 @@ struct CMCfg {
   //   per warp: one output slab in DMMA fragment order ([t][nt][lane][2],
   //   conflict-free 16-byte stores; drained by the producers through the
   //   inverse map s_inv) and, for kCons, one slab of `previous` records.
-  static constexpr int sbuf(int mt) { return (NW * mt / (TJ / 8) + 1) * (TJ + 1) * KCP + KSC * NT * 32; }
+  // WRES: all NK k-steps of W stay resident in shared memory (loaded once per
+  // CTA) instead of riding in every ring slot (cm_wres: where that measured
+  // faster; W <= 40 KB).
+  static constexpr bool WRES = cm_wres(SCH, M) && NK * NT * 256 <= 40 * 1024;
+  static constexpr int WRESN = WRES ? NK * NT * 32 : 0;  // doubles
+  static constexpr int sbuf(int mt) { return (NW * mt / (TJ / 8) + 1) * (TJ + 1) * KCP + (WRES ? 0 : KSC * NT * 32); }
   static constexpr int tail(int mt) {
-    return NW * (mt * NT * 64 + (SCH == kCons ? mt * 8 * O0 : 0)) * 8 + (8 * DO + 8 * NT) * 4 + (8 + 2 * NW) * 8 + 64;
+    return WRESN * 8 + NW * (mt * NT * 64 + (SCH == kCons ? mt * 8 * O0 : 0)) * 8 + (8 * DO + 8 * NT) * 4 +
+           (8 + 2 * NW) * 8 + 64;
   }
   static constexpr bool fits(int mt, int ns) { return ns * sbuf(mt) * 8 + tail(mt) <= SMEM_MAX; }
   // Ring depth: 4 slots only where they leave >= 56 KB of the SM's 256 KB
@@ -96,7 +102,7 @@ struct CMCfg {
   static constexpr int TR = NW * MT / (TJ / 8);    // target rows per tile
   static constexpr int NODES = (TR + 1) * (TJ + 1);
   static constexpr int CBUF = NODES * KCP;
-  static constexpr int WBUF = KSC * NT * 32;
+  static constexpr int WBUF = WRES ? 0 : KSC * NT * 32;
   static constexpr int SBUF = CBUF + WBUF;         // doubles per ring slot
   static constexpr int SLAB = MT * NT * 64;
   static constexpr int PSLAB = SCH == kCons ? MT * 8 * O0 : 0;
@@ -106,7 +112,8 @@ struct CMCfg {
 #else
   static constexpr int NS = fits_soft(MT, 4) ? 4 : (fits(MT, 3) ? 3 : 2);
 #endif
-  static constexpr int EPI0 = NS * SBUF;           // double offset of the slabs
+  static constexpr int WRES0 = NS * SBUF;          // double offset of the resident W
+  static constexpr int EPI0 = WRES0 + WRESN;       // double offset of the slabs
   static constexpr int SMEM = NS * SBUF * 8 + TAIL;
   static constexpr bool PREFETCH_B = NT <= 9;      // W fragments double-buffered in registers too
 };
@@ -463,10 +470,15 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       }
       // W fragments of the chunk (contiguous, 16-byte aligned)
       const int nks = (C::NK - ch * KSC) < KSC ? (C::NK - ch * KSC) : KSC;
-      const double* wsrc = a.wfrag + ch * KSC * NT * 32;
-      double* wb = cb + C::CBUF;
+      if (!C::WRES) {
+        const double* wsrc = a.wfrag + ch * KSC * NT * 32;
+        double* wb = cb + C::CBUF;
 #pragma unroll 1
-      for (int i = pl; i < nks * NT * 16; i += NPL) cm_cp_async16(wb + 2 * i, wsrc + 2 * i);
+        for (int i = pl; i < nks * NT * 16; i += NPL) cm_cp_async16(wb + 2 * i, wsrc + 2 * i);
+      } else if (g == 0) {  // the whole W once; stage 0's cp.async arrive covers it
+#pragma unroll 1
+        for (int i = pl; i < C::NK * NT * 16; i += NPL) cm_cp_async16(smem + C::WRES0 + 2 * i, a.wfrag + 2 * i);
+      }
       mbar_arrive(&full[b]);           // orders this lane's plain shared stores
       mbar_arrive_cp_async(&full[b]);  // fires when this lane's copies have landed
       if (++ch == NCH) {
@@ -527,7 +539,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
     }
     mbar_wait(&full[b], (g / NS) & 1);
     const double* cb = smem + b * C::SBUF;
-    const double* wb = cb + C::CBUF;
+    const double* wb = C::WRES ? smem + C::WRES0 + ch * KSC * NT * 32 : cb + C::CBUF;
     // One chunk of NKS k-steps, software-pipelined: the shared-memory
     // operands of k-step ks+1 (corner values; W fragments when registers
     // allow) are loaded before the DMMAs of k-step ks issue.  FIRST: the
