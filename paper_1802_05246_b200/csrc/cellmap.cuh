@@ -110,12 +110,17 @@ struct CMCfg {
 #ifdef HW_CM_NS
   static constexpr int NS = fits(MT, HW_CM_NS) ? HW_CM_NS : (fits(MT, 3) ? 3 : 2);
 #else
-  static constexpr int NS = fits_soft(MT, 4) ? 4 : (fits(MT, 3) ? 3 : 2);
+  // (conservative m = 4: 3 slots measured 5% faster than 4, tools/gpu_ab.sh)
+  static constexpr int NS = (SCH != kDiss && M == 4) ? 3 : (fits_soft(MT, 4) ? 4 : (fits(MT, 3) ? 3 : 2));
 #endif
   static constexpr int WRES0 = NS * SBUF;          // double offset of the resident W
   static constexpr int EPI0 = WRES0 + WRESN;       // double offset of the slabs
   static constexpr int SMEM = NS * SBUF * 8 + TAIL;
-  static constexpr bool PREFETCH_B = NT <= 9;      // W fragments double-buffered in registers too
+#ifdef HW_CM_PREB
+  static constexpr bool PREFETCH_B = HW_CM_PREB;
+#else
+  static constexpr bool PREFETCH_B = NT <= 8;      // W fragments double-buffered in registers too
+#endif
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
