@@ -59,9 +59,14 @@ struct CMCfg {
   static constexpr int NCH = (NK + KSC - 1) / KSC; // chunks per tile
   static constexpr int KCP = 20;                   // staged doubles per node (= 4 mod 16: conflict-free)
   static constexpr int NW = cm_nw(SCH, M);         // consumer warps (a multiple of 4)
+#ifdef HW_CM_NPW
+  static constexpr int NPW = HW_CM_NPW;
+#else
   static constexpr int NPW = 4;                    // producer warps (one per SM sub-partition)
+#endif
   static constexpr int NTHREADS = 32 * (NW + NPW);
-  static constexpr int TJ = 32;                    // target columns per tile
+  static constexpr int TJ = cm_tj(SCH, M);         // target columns per tile
+  static constexpr int NSMAX = 8;                  // ring slots the barrier arrays hold
   static constexpr int DO = O0 + O1;               // output record per cell
   // setmaxnreg split of the 512 registers per lane of each SM sub-partition
   // (NW / 4 consumer + NPW / 4 producer warps)
@@ -82,7 +87,7 @@ struct CMCfg {
   static constexpr int sbuf(int mt) { return (NW * mt / (TJ / 8) + 1) * (TJ + 1) * KCP + (WRES ? 0 : KSC * NT * 32); }
   static constexpr int tail(int mt) {
     return WRESN * 8 + NW * (mt * NT * 64 + (SCH == kCons ? mt * 8 * O0 : 0)) * 8 + (8 * DO + 8 * NT) * 4 +
-           (8 + 2 * NW) * 8 + 64;
+           (2 * NSMAX + 2 * NW) * 8 + 64;
   }
   static constexpr bool fits(int mt, int ns) { return ns * sbuf(mt) * 8 + tail(mt) <= SMEM_MAX; }
   // Ring depth: 4 slots only where they leave >= 56 KB of the SM's 256 KB
@@ -98,7 +103,11 @@ struct CMCfg {
   // (4 MT + NT) / (MT NT): take MT = 2 where its accumulators (2 MT NT
   // doubles) fit the consumer registers and its slabs fit beside a 2-slot ring.
   // (MT = 3 measured slower than 2 at m = 4: the ring shrinks to 3 slots.)
+#ifdef HW_CM_MT
+  static constexpr int MT = HW_CM_MT;
+#else
   static constexpr int MT = (2 * NT <= 32 && fits(2, 2)) ? 2 : 1;
+#endif
   static constexpr int TR = NW * MT / (TJ / 8);    // target rows per tile
   static constexpr int NODES = (TR + 1) * (TJ + 1);
   static constexpr int CBUF = NODES * KCP;
@@ -109,6 +118,10 @@ struct CMCfg {
   static constexpr int TAIL = tail(MT);
 #ifdef HW_CM_NS
   static constexpr int NS = fits(MT, HW_CM_NS) ? HW_CM_NS : (fits(MT, 3) ? 3 : 2);
+#elif defined(HW_CM_NSDEEP)
+  // deepest ring within the soft limit (at least 2)
+  static constexpr int deepest(int ns) { return ns <= 2 ? 2 : (fits_soft(MT, ns) ? ns : deepest(ns - 1)); }
+  static constexpr int NS = deepest(NSMAX);
 #else
   // (conservative m = 4: 3 slots measured 5% faster than 4, tools/gpu_ab.sh)
   static constexpr int NS = (SCH != kDiss && M == 4) ? 3 : (fits_soft(MT, 4) ? 4 : (fits(MT, 3) ? 3 : 2));
@@ -246,10 +259,10 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
   int* s_inv = reinterpret_cast<int*>(pslabs + NW * C::PSLAB);  // [8 * DO]: output -> fragment slot
   int* s_ocode = s_inv + 8 * C::DO;                              // [NT * 8]: fragment column -> output
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_ocode + 8 * NT + (8 * C::DO + 8 * NT) % 2);
-  uint64_t* full = bars;            // [NS] producers -> consumers: ring slot staged
-  uint64_t* empty = bars + 4;       // [NS] consumers -> producers: ring slot consumed
-  uint64_t* sfull = bars + 8;       // [NW] consumer w -> producer: output slab written
-  uint64_t* sempty = bars + 8 + NW; // [NW] producer -> consumer w: output slab drained
+  uint64_t* full = bars;                  // [NS] producers -> consumers: ring slot staged
+  uint64_t* empty = bars + C::NSMAX;      // [NS] consumers -> producers: ring slot consumed
+  uint64_t* sfull = bars + 2 * C::NSMAX;  // [NW] consumer w -> producer: output slab written
+  uint64_t* sempty = sfull + NW;          // [NW] producer -> consumer w: output slab drained
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   // Inverse fragment map: output q of an M-tile's records, laid out

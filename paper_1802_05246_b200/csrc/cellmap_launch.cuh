@@ -14,6 +14,8 @@ cudaError_t launch_cellmap(const CellMapArgs& a, cudaStream_t st) {
   using C = CMCfg<M, SCH>;
   static_assert(C::SMEM <= 227 * 1024, "stage ring exceeds the 227 KB shared-memory limit");
   static_assert(C::NK <= 64, "per-lane parity bit masks hold at most 64 k-steps");
+  static_assert(C::TJ % 8 == 0 && C::NW % (C::TJ / 8) == 0,
+                "a warp's stacked M-tiles need whole rows of TJ / 8 M-tiles per warp group");
   static_assert(C::NW % 4 == 0 && (C::NPW == 4 || C::NPW == 8) &&
                     (C::NW / 4) * C::CREGS + (C::NPW / 4) * C::PREGS <=
                         65536 / C::NTHREADS / 8 * 8 * ((C::NW + C::NPW) / 4),

@@ -46,7 +46,11 @@ constexpr int cm_nk(int sch, int m) {
 }
 
 // The kernel's staging unit: k-steps per ring chunk.
+#ifdef HW_CM_KSC
+constexpr int cm_ksc() { return HW_CM_KSC; }
+#else
 constexpr int cm_ksc() { return 4; }
+#endif
 
 // Consumer warps per CTA: 12 (three per SM sub-partition, more warps to hide
 // the LDS -> butterfly -> DMMA latency) where that measured faster — the low
@@ -69,6 +73,18 @@ constexpr bool cm_wres(int sch, int m) {
   return HW_CM_WRES;
 #else
   return sch == 0 ? (m == 3 || m == 4) : (m >= 3 && m <= 5);
+#endif
+}
+
+// Target columns per tile (tile = TR rows x TJ columns; the staged halo is
+// (TR + 1)(TJ + 1) nodes).  32 by default; 16 (taller tiles, less halo)
+// where that measured faster (profiles/ab_r01_kernel_knobs.txt).  TJ / 8
+// must divide the consumer warp count (cellmap_launch.cuh asserts it).
+constexpr int cm_tj(int sch, int m) {
+#ifdef HW_CM_TJ
+  return HW_CM_TJ;
+#else
+  return (sch == 0 && m == 4) || (sch != 0 && (m == 4 || m == 8)) ? 16 : 32;
 #endif
 }
 
