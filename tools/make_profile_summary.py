@@ -10,7 +10,8 @@ Writes/updates profiles/ncu_summary.json:
   launch_list[<key>]: per-kernel totals and shares from the
                    `--metrics gpu__time_duration.sum` launch list (cold-cache,
                    serialised: compare shares, not absolutes)
-and copies the condensed CSVs to profiles/ (named per round).
+(copy the launch list and `ncu -i <rep> --page details --csv` to profiles/ beside it,
+named per round: tools/gpu_bench.sh is the command that produced them).
 """
 
 import csv
