@@ -85,8 +85,11 @@ struct CMCfg {
   static constexpr bool WRES = cm_wres(SCH, M) && NK * NT * 256 <= 40 * 1024;
   static constexpr int WRESN = WRES ? NK * NT * 32 : 0;  // doubles
   static constexpr int sbuf(int mt) { return (NW * mt / (TJ / 8) + 1) * (TJ + 1) * KCP + (WRES ? 0 : KSC * NT * 32); }
+  // DIRECT: the consumers store their accumulators straight to HBM (no slab,
+  // no producer drain).
+  static constexpr bool DIRECT = cm_direct(SCH, M);
   static constexpr int tail(int mt) {
-    return WRESN * 8 + NW * (mt * NT * 64 + (SCH == kCons ? mt * 8 * O0 : 0)) * 8 + (8 * DO + 8 * NT) * 4 +
+    return WRESN * 8 + NW * ((DIRECT ? 0 : mt * NT * 64) + (SCH == kCons ? mt * 8 * O0 : 0)) * 8 + (8 * DO + 8 * NT) * 4 +
            (2 * NSMAX + 2 * NW) * 8 + 64;
   }
   static constexpr bool fits(int mt, int ns) { return ns * sbuf(mt) * 8 + tail(mt) <= SMEM_MAX; }
@@ -113,7 +116,7 @@ struct CMCfg {
   static constexpr int CBUF = NODES * KCP;
   static constexpr int WBUF = WRES ? 0 : KSC * NT * 32;
   static constexpr int SBUF = CBUF + WBUF;         // doubles per ring slot
-  static constexpr int SLAB = MT * NT * 64;
+  static constexpr int SLAB = DIRECT ? 0 : MT * NT * 64;
   static constexpr int PSLAB = SCH == kCons ? MT * 8 * O0 : 0;
   static constexpr int TAIL = tail(MT);
 #ifdef HW_CM_NS
@@ -332,6 +335,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
     for (int j = 0; j < NW / C::NPW; ++j) dtile[j] = blockIdx.x, dk[j] = 0;
     auto try_drain = [&]() {
       bool any = false;
+      if constexpr (!C::DIRECT) {  // (DIRECT: the consumers store their own outputs)
 #pragma unroll
       for (int j = 0; j < NW / C::NPW; ++j) {
         const int w = pw + C::NPW * j;
@@ -399,6 +403,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
         dtile[j] += gridDim.x;
         ++dk[j];
         any = true;
+      }
       }
       return any;
     };
@@ -506,7 +511,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       }
     }
     // drain the remaining output slabs
-    while (true) {
+    while (!C::DIRECT) {
       bool left = false;
 #pragma unroll
       for (int j = 0; j < NW / C::NPW; ++j) left |= dtile[j] < ntiles;
@@ -543,7 +548,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       // this tile's epilogue reuses it (and, for kCons, before its `previous`
       // records are staged — contiguous, with cp.async, landing under the
       // last chunk's DMMAs).
-      if (k >= 1) mbar_wait(&sempty[warp], (k - 1) & 1);
+      if (!C::DIRECT && k >= 1) mbar_wait(&sempty[warp], (k - 1) & 1);
       if (SCH == kCons) {
         double* pv = pslabs + warp * C::PSLAB;
 #pragma unroll
@@ -638,7 +643,34 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[b]);  // ring slot b may be refilled
 
-    if (ch == NCH - 1) {
+    if (ch == NCH - 1 && C::DIRECT) {
+      // Epilogue straight to HBM: lane 4 r + j stores outputs 2 j, 2 j + 1 of
+      // every n-tile for cell r of each M-tile.
+      if (SCH == kCons) asm volatile("cp.async.wait_all;\n" ::: "memory");  // `previous` landed
+      const double* pv = pslabs + warp * C::PSLAB;
+      const int r = lane >> 2;
+#pragma unroll
+      for (int t = 0; t < MT; ++t) {
+        int64_t cell0;
+        const int nv = mtile(cg, warp, t, cell0);
+        if (MODE == 3 || r >= nv) continue;
+        double* d0 = a.out0 + (cell0 + r) * C::O0;
+        double* d1 = C::O1 > 0 ? a.out1 + (cell0 + r) * C::O1 : nullptr;
+#pragma unroll
+        for (int n = 0; n < NT; ++n)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int code = s_ocode[n * 8 + 2 * (lane & 3) + i];
+            if (code < 0) continue;
+            const int o = code & 0xffff;
+            if (code >> 16)
+              d1[o] = acc[t][n][i];
+            else
+              d0[o] = SCH == kCons ? acc[t][n][i] - pv[t * 8 * C::O0 + r * C::O0 + o] : acc[t][n][i];
+          }
+      }
+      __syncwarp();
+    } else if (ch == NCH - 1) {
       // Epilogue: accumulators -> this warp's output slab in fragment order; a
       // producer warp drains the slab to HBM while this warp moves on.
 #pragma unroll
@@ -650,6 +682,8 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       if (SCH == kCons) asm volatile("cp.async.wait_all;\n" ::: "memory");  // `previous` landed
       __syncwarp();
       if (lane == 0) mbar_arrive(&sfull[warp]);
+    }
+    if (ch == NCH - 1) {
       ++k;
       ch = 0;
       tile += gridDim.x;

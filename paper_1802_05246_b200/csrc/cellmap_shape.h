@@ -88,4 +88,15 @@ constexpr int cm_tj(int sch, int m) {
 #endif
 }
 
+// Epilogue straight from the accumulators to HBM (no slab, no producer
+// drain): 20% faster at diss m = 2, whose map is so small that the step is
+// HBM-bound, 4-40% slower everywhere else (profiles/ab_r01_kernel_knobs.txt).
+constexpr bool cm_direct(int sch, int m) {
+#ifdef HW_CM_DIRECT
+  return HW_CM_DIRECT;
+#else
+  return sch == 0 && m <= 2;
+#endif
+}
+
 }  // namespace hw

@@ -6,6 +6,11 @@ mkdir -p gpurun_out
 out=gpurun_out/ab.txt
 rm -f $out
 CONFIGS=${AB_CONFIGS:-"diss:2:1024 diss:3:1024 diss:4:1024 diss:5:1024 diss:6:1024 diss:7:1024 diss:8:1024 cons:3:2048:walls cons:4:2048:walls cons:5:2048:walls cons:8:2048:walls"}
+# parity of each variant first (a broken variant's timing means nothing)
+for v in "$@"; do
+  if [ "$v" = default ]; then lib=""; else lib=build_var/$v/libhermb200.so; fi
+  echo "parity [$v]: $(HERMB200_LIB=$lib timeout 300 python -m pytest tests/test_gpu_parity.py tests/test_gpu_slab.py -q -x 2>&1 | tail -1)" >> $out
+done
 for round in 1 2; do
   for v in "$@"; do
     if [ "$v" = default ]; then lib=""; else lib=build_var/$v/libhermb200.so; fi
