@@ -106,8 +106,8 @@ struct CMCfg {
   // (4 MT + NT) / (MT NT): take MT = 2 where its accumulators (2 MT NT
   // doubles) fit the consumer registers and its slabs fit beside a 2-slot ring.
   // (MT = 3 measured slower than 2 at m = 4: the ring shrinks to 3 slots.)
-#ifdef HW_CM_MT
-  static constexpr int MT = HW_CM_MT;
+#ifdef HW_CM_MT  // (A/B builds: where it fits)
+  static constexpr int MT = fits(HW_CM_MT, 2) ? HW_CM_MT : ((2 * NT <= 32 && fits(2, 2)) ? 2 : 1);
 #else
   static constexpr int MT = (2 * NT <= 32 && fits(2, 2)) ? 2 : 1;
 #endif
