@@ -116,6 +116,22 @@ struct CMCfg {
   static constexpr int CBUF = NODES * KCP;
   static constexpr int WBUF = WRES ? 0 : KSC * NT * 32;
   static constexpr int SBUF = CBUF + WBUF;         // doubles per ring slot
+  // bit ch: ring chunk ch lies inside one field whose record length is even
+  // (so a multiple of 4: no padding slots) -> 16-byte staging copies
+  static constexpr unsigned wide_mask() {
+    unsigned mk = 0;
+    for (int ch = 0; ch < NCH && ch < 32; ++ch) {
+      const int s0 = ch * KC, s1 = (s0 + KC < 4 * NK) ? s0 + KC : 4 * NK;
+      const bool in0 = s1 <= K0, in1 = s0 >= K0;
+      if ((in0 && P0 % 2 == 0) || (in1 && P1 > 0 && P1 % 2 == 0)) mk |= 1u << ch;
+    }
+    return mk;
+  }
+#ifdef HW_CM_WIDE
+  static constexpr unsigned WIDE = HW_CM_WIDE ? wide_mask() : 0u;
+#else
+  static constexpr unsigned WIDE = wide_mask();
+#endif
   static constexpr int SLAB = DIRECT ? 0 : MT * NT * 64;
   static constexpr int PSLAB = SCH == kCons ? MT * 8 * O0 : 0;
   static constexpr int TAIL = tail(MT);
@@ -410,6 +426,9 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
 
     int tile = blockIdx.x, ch = 0;
     CMTile t = tile_geo(tile);
+    // 16-byte staging needs 16-byte aligned field bases (even-length records
+    // keep every node and chunk offset even from there)
+    const bool base_al16 = ((reinterpret_cast<uintptr_t>(a.f0.base) | reinterpret_cast<uintptr_t>(a.f1.base)) & 15) == 0;
     for (int g = 0; g < nstages; ++g) {
       const int b = g % NS;
       if (g >= NS) {  // wait for the slot, draining finished output slabs meanwhile
@@ -429,14 +448,36 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       const bool edge = t.s_first < 0 || t.s_first + t.nvr >= a.nx || t.c_first < 0 || t.c_first + t.nvc >= a.ny;
       const bool manual = !a.periodic && edge;  // wall ghosts: reflect after the copies land
       double* dst = cb + q0 * KCP + e;
-      if (pad) {
+      const bool interior = t.nvr == TR && t.nvc == TJ && t.s_first >= a.f0.row0 &&
+                            t.s_first + TR < a.f0.row0 + a.f0.nrows && t.c_first >= 0 && t.c_first + TJ < a.ny;
+      if (MODE != 1 && interior && (C::WIDE >> ch & 1u) && base_al16) {
+        // interior tile, chunk inside one field of even record length (no
+        // padding slots): 16-byte L2-only copies of slot pairs, lane -> (pair
+        // pl % 8, node pl / 8); slots beyond the last k-step are never read
+        constexpr int QW = NPL / 8, NQW = (TJ + QW) / QW;
+        const int e2 = 2 * (pl % 8), qw = pl / 8;
+        if (ch * KC + e2 < 4 * C::NK) {
+          const bool fw = ch * KC >= C::K0;
+          const int pf = fw ? C::P1 : C::P0;
+          const int64_t rowlen = a.ny * pf;
+          const double* src = (fw ? a.f1.base : a.f0.base) + (t.s_first - a.f0.row0) * rowlen +
+                              (t.c_first + qw) * pf + (fw ? ch * KC - C::K0 : ch * KC) + e2;
+          double* dw = cb + qw * KCP + e2;
+#pragma unroll
+          for (int r = 0; r <= TR; ++r) {
+#pragma unroll
+            for (int k = 0; k < NQW; ++k)
+              if (qw + k * QW <= TJ) cm_cp_async16(dw + (r * (TJ + 1) + k * QW) * KCP, src + k * QW * pf);
+            src += rowlen;
+          }
+        }
+      } else if (pad) {
 #pragma unroll 1
         for (int r = 0; r <= TR; ++r)
 #pragma unroll
           for (int k = 0; k < NQ; ++k)
             if (q0 + k * QL <= TJ) dst[(r * (TJ + 1) + k * QL) * KCP] = 0.0;
-      } else if (MODE != 1 && t.nvr == TR && t.nvc == TJ && t.s_first >= a.f0.row0 &&
-                 t.s_first + TR < a.f0.row0 + a.f0.nrows && t.c_first >= 0 && t.c_first + TJ < a.ny) {
+      } else if (MODE != 1 && interior) {
         // interior tile: every staged row is a dense segment of the local slab
         const int pf = f1 ? C::P1 : C::P0;
         const int64_t rowlen = a.ny * pf;

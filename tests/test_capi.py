@@ -57,3 +57,17 @@ def test_bad_geometry_is_an_error_not_a_crash():
     st = L.lib().hw_diss2d_half_step(C.byref(r), C.byref(r), 1, 1, 4, C.byref(g), 0.1, 0.1, 0.1, 1.0, -1, None)
     assert st == -1
     assert "periodicity" in L.lib().hw_last_error().decode()
+
+
+@pytest.mark.gpu
+def test_row_too_long_for_32_bit_staging_offsets_is_an_error():
+    """The 2D kernels stage with 32-bit offsets inside a source row: a row of
+    ny * (m+1)^2 >= 2^31 doubles is refused before any launch (fake device
+    pointers are never touched)."""
+    ny = 90_000_000
+    g = L.Geom2D(2, ny, 0, 1, L.AxisBC(0, 0, 0, 0), L.AxisBC(0, 0, 0, 0), 0, -1)
+    r = L.Rows2D(1 << 20, None, None, 0, 2)
+    st = L.lib().hw_diss2d_half_step(C.byref(r), C.byref(r), 1 << 20, 1 << 20, 4, C.byref(g), 1e-9, 1e-8, 1e-8,
+                                     1.0, -1, None)
+    assert st == -1
+    assert "too long" in L.lib().hw_last_error().decode()

@@ -213,3 +213,35 @@ def test_host_pipelined_path_equals_device_path(per, par):
     assert isinstance(a.u.values, np.ndarray) and a.time == b.time and a.parity == b.parity
     assert np.array_equal(a.u.values, b.u.values.cpu().numpy())
     assert np.array_equal(a.v.values, b.v.values.cpu().numpy())
+
+
+@pytest.mark.parametrize("m", [3, 5])
+def test_unaligned_field_bases_equal_aligned(m):
+    """Fields whose records have even length are staged with 16-byte copies
+    when their base is 16-byte aligned; a view starting one double into its
+    storage must take the 8-byte path and give the same bits."""
+    import torch
+
+    from paper_1802_05246_b200.stepping import diss2d_into
+
+    n = 64
+    grid = hb.Grid2D(0.0, 1.0, 0.0, 1.0, n, n, True)
+    cfg = hb.SchemeConfig(m=m, lam=0.9)
+    g = torch.Generator().manual_seed(m)
+    u = torch.randn((n, n, m + 1, m + 1), generator=g, dtype=torch.float64).cuda()
+    v = torch.randn((n, n, m, m), generator=g, dtype=torch.float64).cuda()
+
+    def shifted(x):  # same values, base address 8 bytes past a 16-byte boundary
+        buf = torch.empty(x.numel() + 1, dtype=x.dtype, device=x.device)
+        y = buf[1:].view(x.shape)
+        y.copy_(x)
+        assert y.data_ptr() % 16 == 8
+        return y
+
+    outs = []
+    for uu, vv in ((u, v), (shifted(u), shifted(v))):
+        ud, vd = torch.empty_like(u), torch.empty_like(v)
+        diss2d_into(uu, vv, ud, vd, grid, hb.PRIMAL, m, cfg, hb.BoundarySpec2D())
+        outs.append((ud, vd))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
