@@ -159,30 +159,91 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ reference (CPU) arm
 
-def cpu_sample(m: int, n: int, rows: int, lam: float = 0.9):
-    """One half step of the numpy restatement of the reference (oracle/,
-    step for step the reference's own numpy ops; pinned bitwise against the
-    reference's golden vectors) on a `rows` x n window of the n x n workload.
-    Returns (seconds, DOF-updates)."""
-    import numpy as np  # noqa: F401
-
+def _window(m: int, n: int, rows: int, r0: int):
+    """Source rows r0 .. r0+rows (inclusive) of the C2 standing wave."""
     from oracle import hermite_oracle as O
 
     h = 1.0 / n
     x = O.nodes(0.0, h, n, True, O.PRIMAL)
-    xw = x[: rows + 1]
+    xw = x[r0: r0 + rows + 1]
     u = O.planewave_data(xw, x, 0.0, m, m, 1, h, h)
     v = O.planewave_data(xw, x, 0.0, m - 1, m - 1, 1, h, h, tder=1)
-    t0 = time.perf_counter()
+    return u, v
+
+
+def _oracle_rows(u, v, m: int, n: int, lam: float = 0.9):
+    """One half step of the numpy restatement of the reference (oracle/, step
+    for step the reference's own numpy ops; pinned bitwise against the
+    reference's golden vectors) for the targets of a source-row window."""
+    import numpy as np
+
+    from oracle import hermite_oracle as O
+
+    h = 1.0 / n
     # rows+1 source rows are "primal with walls" along x locally -> rows targets
     a = O.gather(u, 0, "x", O.PRIMAL, False, None, None)
     du = np.moveaxis(O.gather(a, 2, "y", O.PRIMAL, True, None, None), 1, 2)
     a = O.gather(v, 0, "x", O.PRIMAL, False, None, None)
     dv = np.moveaxis(O.gather(a, 2, "y", O.PRIMAL, True, None, None), 1, 2)
-    uo, vo = O._step_from_corners(du, dv, h, h, m, lam)
-    dt = time.perf_counter() - t0
-    assert uo.shape[0] == rows
-    return dt, rows * n * dof_per_node(m)
+    return O._step_from_corners(du, dv, h, h, m, lam)
+
+
+def _cpu_worker(m, n, rows, r0, rounds, bar, q):
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(1):  # one BLAS thread per worker process
+        u, v = _window(m, n, rows, r0)
+        for _ in range(rounds):
+            bar.wait()
+            t0 = time.time()
+            uo, _ = _oracle_rows(u, v, m, n)
+            t1 = time.time()
+            assert uo.shape[0] == rows
+            q.put((t0, t1))
+
+
+def cpu_workers(m: int, rows: int) -> int:
+    """Worker processes for the CPU legs: every host core, capped so the
+    windows' numpy intermediates (about 45 MB per row at m = 4, scaling as
+    the map size) stay under a quarter of the host's available memory."""
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 64 << 30
+    per = rows * 45e6 * (dof_per_node(m) / 41.0) ** 2
+    return max(1, min(os.cpu_count() or 1, 128, int(0.25 * avail / per)))
+
+
+def cpu_sample(m: int, n: int, rows: int, rounds: int = 1, warm: int = 0):
+    """The reference algorithm on the host: W processes (one BLAS thread
+    each, W = cpu_workers) each take a different `rows` x n window of the n x
+    n workload and run one half step per round, all starting together
+    (barrier).  Returns (per-round wall seconds, DOF-updates per round,
+    W); the first `warm` rounds are untimed."""
+    import multiprocessing as mp
+
+    w = cpu_workers(m, rows)
+    ctx = mp.get_context("spawn")  # (the parent may hold CUDA state and threads)
+    bar = ctx.Barrier(w)
+    q = ctx.Queue()
+    tot = warm + rounds
+    procs = [ctx.Process(target=_cpu_worker, args=(m, n, rows, (k * rows) % max(1, n - rows), tot, bar, q))
+             for k in range(w)]
+    for p in procs:
+        p.start()
+    spans = [q.get(timeout=600) for _ in range(w * tot)]
+    for p in procs:
+        p.join(timeout=60)
+    # rounds are barrier-separated: group the w reports of each round
+    spans.sort()
+    walls = []
+    for r in range(tot):
+        grp = spans[r * w:(r + 1) * w]
+        walls.append(max(t1 for _, t1 in grp) - min(t0 for t0, _ in grp))
+    walls = walls[warm:]
+    return sum(walls) / len(walls), w * rows * n * dof_per_node(m), w
 
 
 def run_reference(args, rank, world):
@@ -190,35 +251,26 @@ def run_reference(args, rank, world):
         return
     m, n = args.m, args.n
     rows = args.ref_rows
-    # bounded: at most 2 warm-up and 10 timed samples of `rows` x n (about 2 s
-    # each at m = 4), whatever --steps / --warmup ask, so the arm ends in well
-    # under a minute; the line reports the sample count it timed
+    # bounded: at most 2 warm-up and 10 timed rounds, each one half step of a
+    # rows x n window per worker process on every host core, whatever --steps
+    # / --warmup ask, so the arm ends in about a minute
     n_warm, n_timed = min(args.warmup, 2), min(args.steps, 10)
-    for _ in range(n_warm):
-        cpu_sample(m, n, rows)
-    tot_t = tot_d = 0.0
-    for _ in range(n_timed):
-        t, d = cpu_sample(m, n, rows)
-        tot_t += t
-        tot_d += d
-    val = tot_d / tot_t / 1e9
-    cores = os.cpu_count()
+    sec, d, w = cpu_sample(m, n, rows, rounds=n_timed, warm=n_warm)
+    val = d / sec / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / n_timed,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec,
         "samples_timed": n_timed,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"2D periodic dissipative Hermite m={m}, {n}x{n}, lambda 0.9 (C2)",
-                   "m": m, "n": n, "sample_rows": rows},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"one half step on a {rows}x{n} window of the {n}x{n} grid per step "
-                                   f"(numpy restatement of hermwave.half_step_2d, OpenBLAS threads default)"},
+                   "m": m, "n": n, "sample_rows_per_worker": rows, "workers": w},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": w, "kind": "port",
+                         "sample": f"{w} processes (1 BLAS thread each) x one half step on a {rows}x{n} window "
+                                   f"of the {n}x{n} grid per step (numpy restatement of hermwave.half_step_2d)"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
-
-# ------------------------------------------------------------------ GPU arm
 
 def main():
     ap = argparse.ArgumentParser()
@@ -228,8 +280,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--m", type=int, default=4)
     ap.add_argument("--n", type=int, default=1024)
-    ap.add_argument("--ref-rows", type=int, default=16)
-    ap.add_argument("--cpu-rows", type=int, default=48)
+    ap.add_argument("--ref-rows", type=int, default=4)
+    ap.add_argument("--cpu-rows", type=int, default=4)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -351,10 +403,11 @@ def main():
     if rank == 0 and world == 1 and not args.no_e2e:
         result["e2e"] = e2e_bench(hb, torch, np, m, n, cfg, min(args.steps, 5))
     if rank == 0 and world == 1 and not args.no_cpu:
-        t_cpu, d_cpu = cpu_sample(m, n, args.cpu_rows)
-        result["cpu_baseline"] = {"value": d_cpu / t_cpu / 1e9, "unit": UNIT, "cores": 1, "kind": "port",
-                                  "sample": f"one half step on a {args.cpu_rows}x{n} window of the {n}x{n} "
-                                            f"grid (numpy restatement of hermwave.half_step_2d)"}
+        t_cpu, d_cpu, w_cpu = cpu_sample(m, n, args.cpu_rows, rounds=2, warm=1)
+        result["cpu_baseline"] = {"value": d_cpu / t_cpu / 1e9, "unit": UNIT, "cores": w_cpu, "kind": "port",
+                                  "sample": f"{w_cpu} processes (1 BLAS thread each) x one half step on a "
+                                            f"{args.cpu_rows}x{n} window of the {n}x{n} grid (numpy restatement "
+                                            f"of hermwave.half_step_2d)"}
     if rank == 0 and world == 1 and not args.no_c3:
         result["c3"] = c3_bench(hb, torch, pk)
     if rank == 0 and world == 1 and not args.no_sweep:
