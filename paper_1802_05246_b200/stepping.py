@@ -64,14 +64,19 @@ def diss2d_into(u, v, ud, vd, grid, parity, m, cfg: SchemeConfig, bc: BoundarySp
     return dt
 
 
-def _diss2d_host_pipelined(uh, vh, grid, parity, m, cfg: SchemeConfig, bc: BoundarySpec2D, nchunks: int = 16):
+def _diss2d_host_pipelined(uh, vh, grid, parity, m, cfg: SchemeConfig, bc: BoundarySpec2D, nchunks: int = 16,
+                           _marks=None):
     """Host arrays in, host arrays out, with the PCIe traffic overlapped: the
     source rows go up in chunks on one stream, each target-row chunk launches
     as soon as the source rows it reads (its flanking rows, periodic wrap or
     wall mirror included) have landed, and its results come back on a third
     stream while the next chunk computes.  Same arithmetic as the one-shot
-    path (the kernel takes a target-row window, hw_geom2d.trow0/ntrows)."""
+    path (the kernel takes a target-row window, hw_geom2d.trow0/ntrows).
+    `_marks` (tools/e2e_timeline.py): a list that receives (label, timing
+    event) pairs for every upload, kernel and download."""
     import torch
+
+    timing = _marks is not None
 
     dev = torch.device("cuda", torch.cuda.current_device())
     nsrc = uh.shape[0]
@@ -91,6 +96,11 @@ def _diss2d_host_pipelined(uh, vh, grid, parity, m, cfg: SchemeConfig, bc: Bound
     off = 0 if parity == PRIMAL else -1
     edges = np.linspace(0, nsrc, nchunks + 1).astype(int)
     ranges = list(zip(edges[:-1], edges[1:]))
+    if off == 0:
+        # from primal data a target chunk also reads the first row of the next
+        # chunk: upload it with this one (one duplicated row per chunk, same
+        # bytes to the same place) so chunk k waits on upload k alone
+        ranges = [(a, min(b + 1, nsrc)) for a, b in ranges]
     if grid.periodic and off < 0:
         # the first target rows read the last source row (periodic wrap):
         # send that row ahead of the chunks so the first launch need not wait
@@ -101,9 +111,11 @@ def _diss2d_host_pipelined(uh, vh, grid, parity, m, cfg: SchemeConfig, bc: Bound
         for a, b in ranges:
             u[a:b].copy_(srcs[0][a:b], non_blocking=True)
             v[a:b].copy_(srcs[1][a:b], non_blocking=True)
-            ev = torch.cuda.Event()
+            ev = torch.cuda.Event(enable_timing=timing)
             ev.record(s_in)
             arrived.append((a, b, ev))
+            if timing:
+                _marks.append((f"up {a}:{b}", ev))
 
     def first_copy(r):  # index of the earliest upload that carries source row r
         return next(i for i, (a, b, _) in enumerate(arrived) if a <= r < b)
@@ -123,12 +135,16 @@ def _diss2d_host_pipelined(uh, vh, grid, parity, m, cfg: SchemeConfig, bc: Bound
         L.check(L.lib().hw_diss2d_half_step(C.byref(rows2d(u)), C.byref(rows2d(v)), ptr(ud) + 8 * int(t0) * shp_u[1] *
                                             (m + 1) ** 2, ptr(vd) + 8 * int(t0) * shp_v[1] * m * m, int(m), C.byref(g),
                                             dt, grid.hx, grid.hy, cfg.speed, cap, comp.cuda_stream), "half_step_2d")
-        done = torch.cuda.Event()
+        done = torch.cuda.Event(enable_timing=timing)
         done.record(comp)
         s_out.wait_event(done)
         with torch.cuda.stream(s_out):
             ho_u[t0:t1].copy_(ud[t0:t1], non_blocking=True)
             ho_v[t0:t1].copy_(vd[t0:t1], non_blocking=True)
+        if timing:
+            back = torch.cuda.Event(enable_timing=True)
+            back.record(s_out)
+            _marks += [(f"kern {t0}:{t1}", done), (f"down {t0}:{t1}", back)]
     s_out.synchronize()
     comp.wait_stream(s_out)
     return dt, ho_u.numpy(), ho_v.numpy()
