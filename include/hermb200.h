@@ -232,6 +232,57 @@ int hw_init_standing2d(double* out, int64_t nx, int64_t ny, int kx, int ky,
                        double ay, double px, double py, double om, double hx,
                        double hy, int tder, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Lower-level batched building blocks (hermwave's re-exported helpers; the
+ * fused steps above do not use them).  Device pointers, C order, stream
+ * ordered.  Element-wise ones are bit-identical to the reference's numpy
+ * expressions; contractions agree to rounding.
+ * ------------------------------------------------------------------------- */
+
+/* interp.py:78-90 apply_interp: data (batch, 2, mu+1) -> out (batch, 2mu+2). */
+int hw_apply_interp(const double* data, double* out, int64_t batch, int mu, void* stream);
+
+/* interp.py:93-111 apply_interp_2d: data (batch, 2, 2, mux+1, muy+1) ->
+ * out (batch, 2mux+2, 2muy+2). */
+int hw_apply_interp_2d(const double* data, double* out, int64_t batch, int mux, int muy, void* stream);
+
+/* dissipative.py:77-106 expand_taylor: cu (batch, lu), cv (batch, lv) ->
+ * tables (batch, lu, smax+1), (batch, lv, smax+1); r = c^2 dt / h^2 as the
+ * caller forms it.  fterm (nullable, (batch, lv, smax)): the forcing terms
+ * h^l dt^s / (l! s!) * f(l, s-1, centers, t), added at stage s. */
+int hw_expand_taylor(const double* cu, const double* cv, double* cu_tab, double* cv_tab, int64_t batch,
+                     int lu, int lv, double dt, double r, int smax, const double* fterm, void* stream);
+
+/* dissipative.py:184-212 expand_taylor_2d: c0 (batch, K, K), d0 (batch, lv,
+ * lv), d1 nullable (batch, K-2, K-2) -> tables (batch, K, K, smax+1); rx, ry
+ * = c^2 dt / h^2 per axis as the caller forms them. */
+int hw_expand_taylor_2d(const double* c0, const double* d0, const double* d1, double* c_tab, double* d_tab,
+                        int64_t batch, int K, int lv, double dt, double rx, double ry, int smax, void* stream);
+
+/* dissipative.py:116-121 eval_series: table (batch, nstages) -> out (batch). */
+int hw_eval_series(const double* table, double* out, int64_t batch, int nstages, double theta, void* stream);
+
+/* conservative.py:115-127 conservative_update_1d: coeffs (batch, 2m+2),
+ * prev/out (batch, m+1), rho = lambda / 2. */
+int hw_cons_update_1d(const double* coeffs, const double* prev, double* out, int64_t batch, int m, double rho,
+                      void* stream);
+
+/* conservative.py:130-136 conservative_update_2d: coeffs (batch, 2m+2,
+ * 2m+2), prev/out (batch, m+1, m+1), rho = c dt / (2 h) per axis; m <= 9. */
+int hw_cons_update_2d(const double* coeffs, const double* prev, double* out, int64_t batch, int m, double rho_x,
+                      double rho_y, void* stream);
+
+/* boundary.py:135-168 pair_sources (dims 1: src (nx, w0) -> out (nt, 2,
+ * w0)) and corner_sources (dims 2: src (nx, ny, w0, w1) -> out (ntx, nty,
+ * 2, 2, w0, w1)), data part; Dirichlet data come from the axis specs. */
+int hw_gather(const double* src, double* out, int dims, int64_t nx, int64_t ny, int w0, int w1, int parity_src,
+              const hw_axis_bc* bcx, const hw_axis_bc* bcy, void* stream);
+
+/* boundary.py:65-98 ghost_data / ghost_data_2d: (batch, n0, n1) blocks
+ * reflected along axis (0: first index, 1: second) across a `kind` wall. */
+int hw_ghost(const double* in, double* out, int64_t batch, int n0, int n1, int axis, int kind, double value,
+             void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -10,6 +10,19 @@ hand-written sm_100a kernels behind the C ABI of include/hermb200.h.
 from .config import BoundarySpec, BoundarySpec2D, SchemeConfig
 from .fields import DUAL, PRIMAL, Field1D, Field2D, FieldPair, Grid1D, Grid2D, TwoLevelState, flip
 from .initdata import planewave_on_grid, standing_wave_on_grid
+from .lowlevel import (
+    PascalTable,
+    apply_interp,
+    apply_interp_2d,
+    conservative_update_1d,
+    conservative_update_2d,
+    eval_series,
+    expand_taylor,
+    expand_taylor_2d,
+    ghost_data,
+    ghost_data_2d,
+    pascal_table,
+)
 from .norms import (
     ErrorReport,
     PlaneWave2D,
@@ -42,6 +55,8 @@ __all__ = [
     "BoundarySpec", "BoundarySpec2D", "SchemeConfig",
     "DUAL", "PRIMAL", "Field1D", "Field2D", "FieldPair", "Grid1D", "Grid2D", "TwoLevelState", "flip",
     "planewave_on_grid", "standing_wave_on_grid",
+    "PascalTable", "apply_interp", "apply_interp_2d", "conservative_update_1d", "conservative_update_2d",
+    "eval_series", "expand_taylor", "expand_taylor_2d", "ghost_data", "ghost_data_2d", "pascal_table",
     "ErrorReport", "PlaneWave2D", "StandingWave2D", "default_npts", "fit_rate", "gauss_rule",
     "dissipative_energy", "dissipative_energy_2d", "conservative_energy",
     "l2_error_field", "l2_error_field_2d", "l2_errors_pair",

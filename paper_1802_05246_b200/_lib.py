@@ -27,6 +27,8 @@ EXPORTS = (
     "hw_cons1d_step", "hw_boot1d", "hw_l2err2d", "hw_l2err1d", "hw_count_nonfinite",
     "hw_init_planewave2d", "hw_init_standing2d", "hw_cell_map_dims", "hw_cell_map_2d",
     "hw_seminorm1d", "hw_cons_energy1d", "hw_seminorm2d",
+    "hw_apply_interp", "hw_apply_interp_2d", "hw_expand_taylor", "hw_expand_taylor_2d", "hw_eval_series",
+    "hw_cons_update_1d", "hw_cons_update_2d", "hw_gather", "hw_ghost",
 )
 
 
@@ -85,6 +87,15 @@ def _declare(lib):
         "hw_count_nonfinite": (_I, [_P, _L, C.POINTER(_L), _P]),
         "hw_seminorm1d": (_I, [_P, _I, _L, _I, C.POINTER(AxisBC), _D, _I, _D, _I, _P, _P, C.POINTER(_D), _P]),
         "hw_cons_energy1d": (_I, [_P, _P, _I, _L, _I, _D, _D, _I, _P, _P, C.POINTER(_D), _P]),
+        "hw_apply_interp": (_I, [_P, _P, _L, _I, _P]),
+        "hw_apply_interp_2d": (_I, [_P, _P, _L, _I, _I, _P]),
+        "hw_expand_taylor": (_I, [_P, _P, _P, _P, _L, _I, _I, _D, _D, _I, _P, _P]),
+        "hw_expand_taylor_2d": (_I, [_P, _P, _P, _P, _P, _L, _I, _I, _D, _D, _D, _I, _P]),
+        "hw_eval_series": (_I, [_P, _P, _L, _I, _D, _P]),
+        "hw_cons_update_1d": (_I, [_P, _P, _P, _L, _I, _D, _P]),
+        "hw_cons_update_2d": (_I, [_P, _P, _P, _L, _I, _D, _D, _P]),
+        "hw_gather": (_I, [_P, _P, _I, _L, _L, _I, _I, _I, C.POINTER(AxisBC), C.POINTER(AxisBC), _P]),
+        "hw_ghost": (_I, [_P, _P, _L, _I, _I, _I, _I, _D, _P]),
         "hw_seminorm2d": (_I, [C.POINTER(Rows2D), _I, _I, C.POINTER(Geom2D), _D, _D, _I, _I, _I, _P, _P,
                                C.POINTER(_D), _P]),
         "hw_init_planewave2d": (_I, [_P, _L, _L, _I, _I, _D, _D, _D, _D, _D, _D, _D, _I, _P]),

@@ -15,6 +15,7 @@
 #include "common.cuh"
 #include "diag.cuh"
 #include "line1d.cuh"
+#include "lowlevel.cuh"
 #include "tables.h"
 
 namespace hw {
@@ -693,6 +694,188 @@ int hw_cons_energy1d(const double* cur, const double* prev, int m, int64_t n_src
     cons_energy1d_kernel<<<(unsigned)nblk, kRedThreads, 0, st>>>(a);
     cuda_check(cudaGetLastError(), "cons_energy1d launch");
     *out_host = reduce_partials(part.p, nblk, st);
+  });
+}
+
+// ------------------------------------------------------------------ lower-level API (lowlevel.cuh)
+// A host table uploaded for one call (stream-ordered; freed after the launch).
+struct CallTable {
+  double* p = nullptr;
+  cudaStream_t st;
+  CallTable(const std::vector<double>& h, cudaStream_t s) : st(s) {
+    cuda_check(cudaMallocAsync((void**)&p, h.size() * sizeof(double), st), "cudaMallocAsync");
+    cuda_check(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, st),
+               "cudaMemcpyAsync");
+  }
+  ~CallTable() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
+
+static unsigned ll_blocks(int64_t n) { return (unsigned)((n + 127) / 128); }
+
+int hw_apply_interp(const double* data, double* out, int64_t batch, int mu, void* stream) {
+  return guard([&] {
+    HW_CHECK(mu >= 0 && mu <= kMaxOrder, "interpolation order out of range");
+    HW_CHECK(batch >= 0 && (batch == 0 || (data && out)), "null pointer");
+    if (batch == 0) return;
+    cudaStream_t st = (cudaStream_t)stream;
+    const CallTable M(hermite_matrix(mu), st);
+    const int n = 2 * mu + 2;
+    apply_interp_kernel<<<ll_blocks(batch * n), 128, 0, st>>>(data, out, batch, n, M.p);
+    cuda_check(cudaGetLastError(), "apply_interp launch");
+  });
+}
+
+int hw_apply_interp_2d(const double* data, double* out, int64_t batch, int mux, int muy, void* stream) {
+  return guard([&] {
+    HW_CHECK(mux >= 0 && muy >= 0 && mux <= kMaxOrder && muy <= kMaxOrder, "interpolation order out of range");
+    HW_CHECK(batch >= 0 && (batch == 0 || (data && out)), "null pointer");
+    if (batch == 0) return;
+    cudaStream_t st = (cudaStream_t)stream;
+    const CallTable Mx(hermite_matrix(mux), st), My(hermite_matrix(muy), st);
+    apply_interp2d_kernel<<<ll_blocks(batch * (2 * mux + 2)), 128, 0, st>>>(data, out, batch, mux, muy, Mx.p, My.p);
+    cuda_check(cudaGetLastError(), "apply_interp_2d launch");
+  });
+}
+
+int hw_expand_taylor(const double* cu, const double* cv, double* cu_tab, double* cv_tab, int64_t batch, int lu,
+                     int lv, double dt, double r, int smax, const double* fterm, void* stream) {
+  return guard([&] {
+    HW_CHECK(lu >= 1 && lv >= 0 && lv <= lu && smax >= 0, "table sizes out of range");
+    HW_CHECK(batch >= 0 && (batch == 0 || (cu && cu_tab && (lv == 0 || (cv && cv_tab)))), "null pointer");
+    if (batch == 0) return;
+    cudaStream_t st = (cudaStream_t)stream;
+    expand_taylor_kernel<<<ll_blocks(batch), 128, 0, st>>>(cu, cv, cu_tab, cv_tab, batch, lu, lv, dt, r, smax, fterm);
+    cuda_check(cudaGetLastError(), "expand_taylor launch");
+  });
+}
+
+int hw_expand_taylor_2d(const double* c0, const double* d0, const double* d1, double* c_tab, double* d_tab,
+                        int64_t batch, int K, int lv, double dt, double rx, double ry, int smax, void* stream) {
+  return guard([&] {
+    HW_CHECK(K >= 2 && lv >= 0 && lv <= K && smax >= 0, "table sizes out of range");
+    HW_CHECK(batch >= 0 && (batch == 0 || (c0 && d0 && c_tab && d_tab)), "null pointer");
+    if (batch == 0) return;
+    cudaStream_t st = (cudaStream_t)stream;
+    expand_taylor2d_kernel<<<ll_blocks(batch), 128, 0, st>>>(c0, d0, d1, c_tab, d_tab, batch, K, lv, dt, rx, ry, smax);
+    cuda_check(cudaGetLastError(), "expand_taylor_2d launch");
+  });
+}
+
+int hw_eval_series(const double* table, double* out, int64_t batch, int nstages, double theta, void* stream) {
+  return guard([&] {
+    HW_CHECK(nstages >= 1, "empty series");
+    HW_CHECK(batch >= 0 && (batch == 0 || (table && out)), "null pointer");
+    if (batch == 0) return;
+    cudaStream_t st = (cudaStream_t)stream;
+    eval_series_kernel<<<ll_blocks(batch), 128, 0, st>>>(table, out, batch, nstages, theta);
+    cuda_check(cudaGetLastError(), "eval_series launch");
+  });
+}
+
+// conservative.py:77-84 _update_matrix_1d: W[k][j] = C(j, k) rho^(j-k), j = k, k+2, ...
+int hw_cons_update_1d(const double* coeffs, const double* prev, double* out, int64_t batch, int m, double rho,
+                      void* stream) {
+  return guard([&] {
+    HW_CHECK(m >= 1 && m < kMaxOrder, "method order out of range");
+    HW_CHECK(batch >= 0 && (batch == 0 || (coeffs && prev && out)), "null pointer");
+    if (batch == 0) return;
+    const int nj = 2 * m + 2;
+    std::vector<double> w((size_t)(m + 1) * nj, 0.0);
+    for (int k = 0; k <= m; ++k)
+      for (int j = k; j < nj; j += 2) w[(size_t)k * nj + j] = binom(j, k) * std::pow(rho, (double)(j - k));
+    cudaStream_t st = (cudaStream_t)stream;
+    const CallTable W(w, st);
+    cons_update_kernel<<<ll_blocks(batch * (m + 1)), 128, 0, st>>>(coeffs, prev, out, batch, m + 1, nj, W.p);
+    cuda_check(cudaGetLastError(), "conservative_update_1d launch");
+  });
+}
+
+// conservative.py:87-112 _update_tensor_2d: WT[k][l][a][b] at a = k + 2i, b = l + 2j is
+// float(C(a,k) C(b,l) C(i+j,i) / C(2i+2j,2i)) rho_x^(2i) rho_y^(2j)
+int hw_cons_update_2d(const double* coeffs, const double* prev, double* out, int64_t batch, int m, double rho_x,
+                      double rho_y, void* stream) {
+  return guard([&] {
+    // (the exact-integer numerator below stays under 2^53 up to m = 9)
+    HW_CHECK(m >= 1 && m <= 9, "2D conservative update order must be in [1, 9]");
+    HW_CHECK(batch >= 0 && (batch == 0 || (coeffs && prev && out)), "null pointer");
+    if (batch == 0) return;
+    const int kk = 2 * m + 2, nq = (m + 1) * (m + 1), nj = kk * kk;
+    std::vector<double> w((size_t)nq * nj, 0.0);
+    for (int k = 0; k <= m; ++k)
+      for (int l = 0; l <= m; ++l)
+        for (int i = 0; k + 2 * i <= 2 * m + 1; ++i)
+          for (int j = 0; l + 2 * j <= 2 * m + 1; ++j) {
+            const int a = k + 2 * i, b = l + 2 * j;
+            // the numerator (< 2^53) and denominator are exact doubles: one correctly rounded division
+            const double num = binom(a, k) * binom(b, l) * binom(i + j, i);
+            const double frac = num / binom(2 * i + 2 * j, 2 * i);
+            w[(size_t)(k * (m + 1) + l) * nj + a * kk + b] =
+                frac * std::pow(rho_x, (double)(2 * i)) * std::pow(rho_y, (double)(2 * j));
+          }
+    cudaStream_t st = (cudaStream_t)stream;
+    const CallTable W(w, st);
+    cons_update_kernel<<<ll_blocks(batch * nq), 128, 0, st>>>(coeffs, prev, out, batch, nq, nj, W.p);
+    cuda_check(cudaGetLastError(), "conservative_update_2d launch");
+  });
+}
+
+int hw_gather(const double* src, double* out, int dims, int64_t nx, int64_t ny, int w0, int w1, int parity_src,
+              const hw_axis_bc* bcx, const hw_axis_bc* bcy, void* stream) {
+  return guard([&] {
+    HW_CHECK(dims == 1 || dims == 2, "dims must be 1 or 2");
+    HW_CHECK(bcx && (dims == 1 || bcy), "null boundary spec");
+    HW_CHECK(w0 >= 1 && w1 >= 1 && (dims == 2 || w1 == 1), "block widths out of range");
+    HW_CHECK(parity_src == HW_PRIMAL || parity_src == HW_DUAL, "unknown parity");
+    const int periodic = bcx->left_kind == HW_PERIODIC;
+    check_bc_axis(*bcx, periodic);
+    if (dims == 2) check_bc_axis(*bcy, periodic);
+    HW_CHECK(nx >= 1 && (dims == 1 ? ny == 1 : ny >= 1), "node counts out of range");
+    GatherArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.src = src;
+    a.out = out;
+    a.nx = nx;
+    a.ny = ny;
+    a.ntx = target_count(nx, parity_src, periodic);
+    a.nty = dims == 2 ? target_count(ny, parity_src, periodic) : 1;
+    a.w0 = w0;
+    a.w1 = w1;
+    a.off = src_offset(parity_src);
+    a.periodic = periodic;
+    a.dims = dims;
+    if (!periodic) {
+      a.kxl = bcx->left_kind;
+      a.kxh = bcx->right_kind;
+      a.gxl = bcx->left_value;
+      a.gxh = bcx->right_value;
+      if (dims == 2) {
+        a.kyl = bcy->left_kind;
+        a.kyh = bcy->right_kind;
+        a.gyl = bcy->left_value;
+        a.gyh = bcy->right_value;
+      }
+    }
+    const int64_t n = a.ntx * a.nty * (dims == 2 ? 4 : 2) * w0 * w1;
+    if (n == 0) return;
+    HW_CHECK(src && out, "null pointer");
+    gather_kernel<<<ll_blocks(n), 128, 0, (cudaStream_t)stream>>>(a);
+    cuda_check(cudaGetLastError(), "gather launch");
+  });
+}
+
+int hw_ghost(const double* in, double* out, int64_t batch, int n0, int n1, int axis, int kind, double value,
+             void* stream) {
+  return guard([&] {
+    HW_CHECK(kind == HW_DIRICHLET0 || kind == HW_NEUMANN0, "ghosts reflect across dirichlet0 or neumann0 walls");
+    HW_CHECK(axis == 0 || axis == 1, "axis must be 0 or 1");
+    HW_CHECK(n0 >= 1 && n1 >= 1 && batch >= 0, "sizes out of range");
+    const int64_t n = batch * n0 * n1;
+    if (n == 0) return;
+    HW_CHECK(in && out, "null pointer");
+    ghost_kernel<<<ll_blocks(n), 128, 0, (cudaStream_t)stream>>>(in, out, batch, n0, n1, axis, kind, value);
+    cuda_check(cudaGetLastError(), "ghost launch");
   });
 }
 
