@@ -45,6 +45,10 @@ struct CellMapArgs {
   double gxl, gxh, gyl, gyh;   // Dirichlet data, field 0 only
 };
 
+#ifndef HW_CM_SLEEP
+#define HW_CM_SLEEP 64  // producer back-off (ns) while its ring slot is busy and no slab is ready
+#endif
+
 template <int M, int SCH>
 struct CMCfg {
   static constexpr int W0 = cm_win(SCH, M, 0), W1 = cm_win(SCH, M, 1);
@@ -435,7 +439,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
         while (true) {
           int ok = lane == 0 ? (int)mbar_test(&empty[b], ((g / NS) - 1) & 1) : 0;
           if (__shfl_sync(0xffffffffu, ok, 0)) break;
-          if (!try_drain()) __nanosleep(64);
+          if (!try_drain()) __nanosleep(HW_CM_SLEEP);
         }
       } else {
         try_drain();
@@ -557,7 +561,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
 #pragma unroll
       for (int j = 0; j < NW / C::NPW; ++j) left |= dtile[j] < ntiles;
       if (!left) break;
-      if (!try_drain()) __nanosleep(64);
+      if (!try_drain()) __nanosleep(HW_CM_SLEEP);
     }
     return;
   }
