@@ -15,7 +15,7 @@ row per half step with its ring neighbour (torch.distributed P2P over NCCL).
 
 Extra keys beside the contract's: "c3" (conservative m=5, 2048^2,
 Dirichlet/Neumann walls — BASELINE configs[2]) and "sweep" (dissipative
-m=4..8 at ~2^30 DOF per level — configs[3]), both device resident.
+m=2..8 at ~2^30 DOF per level — configs[3]), both device resident.
 """
 
 from __future__ import annotations
@@ -494,11 +494,14 @@ def c3_bench(hb, torch, pk):
 
 
 def sweep(hb, torch, pk):
-    """Config C4: dissipative m = 4..8 at ~2^30 DOF per level (device resident)."""
+    """Config C4: dissipative m = 2..8 at ~2^30 DOF per level (device
+    resident); each entry carries both roofline fractions (DMMA by SURVEY's
+    F_alg, HBM by 16 B/DOF) and the binding one: SURVEY §8d puts the
+    HBM / FP64 crossover between m = 2 and 3."""
     from paper_1802_05246_b200.stepping import diss2d_into
 
     out = {}
-    for m in range(4, 9):
+    for m in range(2, 9):
         n = SWEEP_N[m]
         grid = hb.Grid2D(0.0, 1.0, 0.0, 1.0, n, n, True)
         cfg = hb.SchemeConfig(m=m, lam=0.9)
@@ -524,6 +527,8 @@ def sweep(hb, torch, pk):
                         "frac_dmma_peak": tf / pk["dmma_tflops"],
                         "issued_dmma_frac": issued * n * n / sec / 1e12 / pk["dmma_tflops"],
                         "hbm_frac": 16 * n * n * dof_per_node(m) / sec / 1e9 / pk["hbm_gbs"]}
+        ai = f_alg_diss(m) / (16 * dof_per_node(m))  # flop / B
+        out[f"m{m}"]["bound"] = "hbm" if ai < pk["dmma_tflops"] * 1e3 / pk["hbm_gbs"] else "tensor"
         del u, v, bufs
         torch.cuda.empty_cache()
     return out
