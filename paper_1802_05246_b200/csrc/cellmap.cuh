@@ -75,7 +75,8 @@ struct CMCfg {
   // setmaxnreg split of the 512 registers per lane of each SM sub-partition
   // (NW / 4 consumer + NPW / 4 producer warps)
   static constexpr int PREGS = NPW == 8 ? 56 : 72;
-  static constexpr int CREGS0 = ((512 - (NPW / 4) * PREGS) / (NW / 4)) / 8 * 8;
+  static constexpr int LREGS = 65536 / NTHREADS / 8 * 8 * ((NW + NPW) / 4);  // per lane slot at launch
+  static constexpr int CREGS0 = ((LREGS - (NPW / 4) * PREGS) / (NW / 4)) / 8 * 8;
   static constexpr int CREGS = CREGS0 > 232 ? 232 : CREGS0;
   static constexpr int SMEM_MAX = 227 * 1024;
   // Shared memory for MT M-tiles per consumer warp and an NS-slot ring:

@@ -60,6 +60,8 @@ constexpr int cm_ksc() { return 4; }
 constexpr int cm_nw(int sch, int m) {
 #ifdef HW_CM_NW
   return HW_CM_NW;
+#elif defined(HW_CM_NW_LOW)  // (A/B builds: m <= 2 only)
+  return m <= 2 ? HW_CM_NW_LOW : ((m <= 3 || (sch != 0 && m == 5) || (sch == 0 && (m == 6 || m == 7))) ? 12 : 8);
 #else
   return (m <= 3 || (sch != 0 && m == 5) || (sch == 0 && (m == 6 || m == 7))) ? 12 : 8;
 #endif
