@@ -91,8 +91,11 @@ struct CMCfg {
   static constexpr int WRESN = WRES ? NK * NT * 32 : 0;  // doubles
   static constexpr int sbuf(int mt) { return (NW * mt / (TJ / 8) + 1) * (TJ + 1) * KCP + (WRES ? 0 : KSC * NT * 32); }
   // DIRECT: the consumers store their accumulators straight to HBM (no slab,
-  // no producer drain).
+  // no producer drain).  SELF: each consumer warp drains its own slab
+  // (fragment-order stores, record-order coalesced copy-out), no handoff.
   static constexpr bool DIRECT = cm_direct(SCH, M);
+  static constexpr bool SELF = cm_self(SCH, M) && !DIRECT;
+  static constexpr bool OWN = DIRECT || SELF;  // the consumers write HBM themselves
   static constexpr int tail(int mt) {
     return WRESN * 8 + NW * ((DIRECT ? 0 : mt * NT * 64) + (SCH == kCons ? mt * 8 * O0 : 0)) * 8 + (8 * DO + 8 * NT) * 4 +
            (2 * NSMAX + 2 * NW) * 8 + 64;
@@ -357,7 +360,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
     for (int j = 0; j < NW / C::NPW; ++j) dtile[j] = blockIdx.x, dk[j] = 0;
     auto try_drain = [&]() {
       bool any = false;
-      if constexpr (!C::DIRECT) {  // (DIRECT: the consumers store their own outputs)
+      if constexpr (!C::OWN) {  // (DIRECT / SELF: the consumers store their own outputs)
 #pragma unroll
       for (int j = 0; j < NW / C::NPW; ++j) {
         const int w = pw + C::NPW * j;
@@ -558,7 +561,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       }
     }
     // drain the remaining output slabs
-    while (!C::DIRECT) {
+    while (!C::OWN) {
       bool left = false;
 #pragma unroll
       for (int j = 0; j < NW / C::NPW; ++j) left |= dtile[j] < ntiles;
@@ -595,7 +598,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       // this tile's epilogue reuses it (and, for kCons, before its `previous`
       // records are staged — contiguous, with cp.async, landing under the
       // last chunk's DMMAs).
-      if (!C::DIRECT && k >= 1) mbar_wait(&sempty[warp], (k - 1) & 1);
+      if (!C::OWN && k >= 1) mbar_wait(&sempty[warp], (k - 1) & 1);
       if (SCH == kCons) {
         double* pv = pslabs + warp * C::PSLAB;
 #pragma unroll
@@ -728,7 +731,27 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
               make_double2(acc[t][n][0], acc[t][n][1]);
       if (SCH == kCons) asm volatile("cp.async.wait_all;\n" ::: "memory");  // `previous` landed
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sfull[warp]);
+      if constexpr (C::SELF) {
+        // drain it ourselves: record order, consecutive lanes on consecutive doubles
+        const double* pv = pslabs + warp * C::PSLAB;
+#pragma unroll
+        for (int t = 0; t < MT; ++t) {
+          int64_t cell0;
+          const int nv = mtile(cg, warp, t, cell0);
+          if (MODE == 3 || nv == 0) continue;
+          const double* s0 = slab + t * NT * 64;
+          double* o0 = a.out0 + cell0 * C::O0;
+          for (int q = lane; q < nv * C::O0; q += 32)
+            o0[q] = SCH == kCons ? s0[s_inv[q]] - pv[t * 8 * C::O0 + q] : s0[s_inv[q]];
+          if (C::O1 > 0) {
+            double* o1 = a.out1 + cell0 * C::O1;
+            for (int q = lane; q < nv * C::O1; q += 32) o1[q] = s0[s_inv[8 * C::O0 + q]];
+          }
+        }
+        __syncwarp();
+      } else {
+        if (lane == 0) mbar_arrive(&sfull[warp]);
+      }
     }
     if (ch == NCH - 1) {
       ++k;

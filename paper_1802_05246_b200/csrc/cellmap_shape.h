@@ -101,4 +101,15 @@ constexpr bool cm_direct(int sch, int m) {
 #endif
 }
 
+// Each consumer warp drains its own output slab (no producer handoff):
+// measured 7% faster at diss m = 3 and 3% at cons m = 3, slower from m = 4 up
+// where the producers' otherwise idle issue slots are worth more.
+constexpr bool cm_self(int sch, int m) {
+#ifdef HW_CM_SELF
+  return HW_CM_SELF;
+#else
+  return sch != 2 && m == 3;
+#endif
+}
+
 }  // namespace hw
