@@ -114,11 +114,12 @@ struct CMCfg {
   // (4 MT + NT) / (MT NT): take MT = 2 where its accumulators (2 MT NT
   // doubles) fit the consumer registers and its slabs fit beside a 2-slot ring.
   // (MT = 3 measured slower than 2 at m = 4: the ring shrinks to 3 slots.)
-#ifdef HW_CM_MT  // (A/B builds: where it fits)
-  static constexpr int MT = fits(HW_CM_MT, 3) ? HW_CM_MT : ((2 * NT <= 32 && fits(2, 2)) ? 2 : 1);
-#else
   // (conservative m = 3: three M-tiles with a 2-slot ring measured 6% faster)
-  static constexpr int MT = (SCH == kCons && M == 3) ? 3 : ((2 * NT <= 32 && fits(2, 2)) ? 2 : 1);
+  static constexpr int MT0 = (SCH == kCons && M == 3) ? 3 : ((2 * NT <= 32 && fits(2, 2)) ? 2 : 1);
+#ifdef HW_CM_MT  // (A/B builds: where it fits)
+  static constexpr int MT = cm_knob(SCH, M) && fits(HW_CM_MT, 2) ? HW_CM_MT : MT0;
+#else
+  static constexpr int MT = MT0;
 #endif
   static constexpr int TR = NW * MT / (TJ / 8);    // target rows per tile
   static constexpr int NODES = (TR + 1) * (TJ + 1);
@@ -145,7 +146,8 @@ struct CMCfg {
   static constexpr int PSLAB = SCH == kCons ? MT * 8 * O0 : 0;
   static constexpr int TAIL = tail(MT);
 #ifdef HW_CM_NS
-  static constexpr int NS = fits(MT, HW_CM_NS) ? HW_CM_NS : (fits(MT, 3) ? 3 : 2);
+  static constexpr int NS = cm_knob(SCH, M) && fits(MT, HW_CM_NS) ? HW_CM_NS :
+      ((SCH != kDiss && M == 4) ? 3 : (fits_soft(MT, 4) ? 4 : (fits(MT, 3) ? 3 : 2)));
 #elif defined(HW_CM_NSDEEP)
   // deepest ring within the soft limit (at least 2)
   static constexpr int deepest(int ns) { return ns <= 2 ? 2 : (fits_soft(MT, ns) ? ns : deepest(ns - 1)); }
@@ -158,7 +160,7 @@ struct CMCfg {
   static constexpr int EPI0 = WRES0 + WRESN;       // double offset of the slabs
   static constexpr int SMEM = NS * SBUF * 8 + TAIL;
 #ifdef HW_CM_PREB
-  static constexpr bool PREFETCH_B = HW_CM_PREB;
+  static constexpr bool PREFETCH_B = cm_knob(SCH, M) ? HW_CM_PREB : NT <= 8;
 #else
   static constexpr bool PREFETCH_B = NT <= 8;      // W fragments double-buffered in registers too
 #endif

@@ -45,6 +45,19 @@ constexpr int cm_nk(int sch, int m) {
   return (cm_k0(sch, m) + (cm_win(sch, m, 1) * cm_win(sch, m, 1) + 3) / 4 * 4) / 4;
 }
 
+// A/B builds (tools/build_variant.sh): -DHW_CM_<KNOB>=v overrides one of the
+// per-order choices below, for every order or, with -DHW_CM_KNOB_M=m (and
+// -DHW_CM_KNOB_SCH=s), for one.
+constexpr bool cm_knob(int sch, int m) {
+#ifdef HW_CM_KNOB_M
+  if (m != HW_CM_KNOB_M) return false;
+#endif
+#ifdef HW_CM_KNOB_SCH
+  if (sch != HW_CM_KNOB_SCH) return false;
+#endif
+  return sch >= 0 && m >= 0;
+}
+
 // The kernel's staging unit: k-steps per ring chunk.
 #ifdef HW_CM_KSC
 constexpr int cm_ksc() { return HW_CM_KSC; }
@@ -59,12 +72,9 @@ constexpr int cm_ksc() { return 4; }
 // budget of two warps per sub-partition win (tools/gpu_perf.sh, round 1).
 constexpr int cm_nw(int sch, int m) {
 #ifdef HW_CM_NW
-  return HW_CM_NW;
-#elif defined(HW_CM_NW_LOW)  // (A/B builds: m <= 2 only)
-  return m <= 2 ? HW_CM_NW_LOW : ((m <= 3 || (sch != 0 && m == 5) || (sch == 0 && (m == 6 || m == 7))) ? 12 : 8);
-#else
-  return (m <= 3 || (sch != 0 && m == 5) || (sch == 0 && (m == 6 || m == 7))) ? 12 : 8;
+  if (cm_knob(sch, m)) return HW_CM_NW;
 #endif
+  return (m <= 3 || (sch != 0 && m == 5) || (sch == 0 && (m == 6 || m == 7))) ? 12 : 8;
 }
 
 // W resident in shared memory for the whole kernel instead of staged per
@@ -72,10 +82,9 @@ constexpr int cm_nw(int sch, int m) {
 // neutral at diss m = 5, 5% slower at m = 2 (tools/cellmap_probe, round 1).
 constexpr bool cm_wres(int sch, int m) {
 #ifdef HW_CM_WRES
-  return HW_CM_WRES;
-#else
-  return sch == 0 ? (m == 3 || m == 4) : (m >= 3 && m <= 5);
+  if (cm_knob(sch, m)) return HW_CM_WRES;
 #endif
+  return sch == 0 ? (m == 3 || m == 4) : (m >= 3 && m <= 5);
 }
 
 // Target columns per tile (tile = TR rows x TJ columns; the staged halo is
@@ -84,10 +93,9 @@ constexpr bool cm_wres(int sch, int m) {
 // must divide the consumer warp count (cellmap_launch.cuh asserts it).
 constexpr int cm_tj(int sch, int m) {
 #ifdef HW_CM_TJ
-  return HW_CM_TJ;
-#else
-  return (sch == 0 && m == 4) || (sch != 0 && (m == 4 || m == 8)) ? 16 : 32;
+  if (cm_knob(sch, m)) return HW_CM_TJ;
 #endif
+  return (sch == 0 && m == 4) || (sch != 0 && (m == 4 || m == 8)) ? 16 : 32;
 }
 
 // Epilogue straight from the accumulators to HBM (no slab, no producer
@@ -95,10 +103,9 @@ constexpr int cm_tj(int sch, int m) {
 // HBM-bound, 4-40% slower everywhere else (profiles/ab_r01_kernel_knobs.txt).
 constexpr bool cm_direct(int sch, int m) {
 #ifdef HW_CM_DIRECT
-  return HW_CM_DIRECT;
-#else
-  return sch == 0 && m <= 2;
+  if (cm_knob(sch, m)) return HW_CM_DIRECT;
 #endif
+  return sch == 0 && m <= 2;
 }
 
 // Each consumer warp drains its own output slab (no producer handoff):
@@ -106,10 +113,9 @@ constexpr bool cm_direct(int sch, int m) {
 // where the producers' otherwise idle issue slots are worth more.
 constexpr bool cm_self(int sch, int m) {
 #ifdef HW_CM_SELF
-  return HW_CM_SELF;
-#else
-  return sch != 2 && m == 3;
+  if (cm_knob(sch, m)) return HW_CM_SELF;
 #endif
+  return sch != 2 && m == 3;
 }
 
 }  // namespace hw
