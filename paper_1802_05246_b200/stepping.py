@@ -187,12 +187,12 @@ def advance_2d(state: FieldPair, cfg: SchemeConfig, bc: BoundarySpec2D, nhalf: i
     grid = state.u.grid
     if state.u.orders != (m, m):
         raise ValueError(f"state carries orders {state.u.orders}, config wants ({m}, {m})")
+    if nhalf <= 0:
+        return state
     st = Staging(state.u.values, state.v.values)
     u = st.to_dev(state.u.values)
     v = st.to_dev(state.v.values)
     parity, t = state.parity, state.time
-    if nhalf <= 0:
-        return state
     owned = st.host  # staged copies of host inputs may be overwritten
     dst = {}
     for _ in range(nhalf):
