@@ -1,0 +1,87 @@
+"""BASELINE config C1 end to end on the device against the reference's own run
+(tests/golden/c1.npz from tests/golden/make_golden_c1.py): 1D periodic
+dissipative m=3, CFL 0.9, sin(x) cos(t) on [0, 2 pi] to t ~ 1.  Per-level
+(u, u_x, v) L2 errors, the fitted orders, and at n_x = 200 the final state to
+the north star's tolerance (max-norm relative difference 1e-12)."""
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "c1.npz")
+M, LAM, T = 3, 0.9, 1.0
+
+
+def _run(n):
+    import torch
+
+    import paper_1802_05246_b200 as hb
+    from paper_1802_05246_b200.studies import scale_cols, sine_derivs
+
+    grid = hb.Grid1D(0.0, 2.0 * math.pi, n, True)
+    h = grid.h
+    cfg = hb.SchemeConfig(m=M, lam=LAM)
+    dt = cfg.dt(h)
+    u0 = torch.from_numpy(scale_cols(sine_derivs(grid.nodes(hb.PRIMAL), M, 0.0), h)).cuda()
+    v0 = torch.zeros((n, M), dtype=torch.float64, device="cuda")
+    pair = hb.FieldPair(hb.Field1D(grid, hb.PRIMAL, 0.0, u0), hb.Field1D(grid, hb.PRIMAL, 0.0, v0))
+    bc = hb.BoundarySpec()
+    nhalf = round(2.0 * T / dt)
+    for _ in range(nhalf):
+        pair = hb.half_step_1d(pair, cfg, bc)
+    t = pair.u.time
+    errs = hb.l2_errors_pair(pair, lambda x: np.sin(x) * math.cos(t), lambda x: np.cos(x) * math.cos(t),
+                             lambda x: -np.sin(x) * math.sin(t), bc)
+    return pair, nhalf, np.array(errs)
+
+
+@pytest.mark.gpu
+def test_c1_ladder_errors_and_orders_match_reference():
+    import paper_1802_05246_b200 as hb
+
+    with np.load(GOLD) as z:
+        g = {k: z[k] for k in z.files}
+    errs, hs = [], []
+    for n in g["ladder"]:
+        pair, nhalf, e = _run(int(n))
+        assert nhalf == int(g[f"n{n}/nhalf"]) and pair.u.time == float(g[f"n{n}/time"])
+        errs.append(e)
+        hs.append(pair.u.grid.h)
+    errs = np.array(errs)
+    # errors of 5e-6 .. 3e-9 agree to rounding (absolute 1e-14)
+    np.testing.assert_allclose(errs, g["errors"], rtol=1e-9, atol=1e-14)
+    rates = np.array([hb.fit_rate(np.array(hs), errs[:, j]) for j in range(3)])
+    np.testing.assert_allclose(rates, g["rates"], rtol=0, atol=1e-6)
+
+
+@pytest.mark.gpu
+def test_c1_nx200_final_state_matches_reference():
+    with np.load(GOLD) as z:
+        g = {k: z[k] for k in z.files}
+    pair, nhalf, e = _run(200)
+    assert nhalf == int(g["n200/nhalf"]) == 71 and pair.u.time == float(g["n200/time"])
+    # the north star's "about 1e-12" max-norm relative difference, calibrated by
+    # the reference algorithm's own sensitivity (oracle, 1-ulp input
+    # perturbation, same 71 half steps: SURVEY App. A.4)
+    from oracle import hermite_oracle as O
+    from paper_1802_05246_b200.studies import scale_cols, sine_derivs
+
+    n, h = 200, 2.0 * math.pi / 200
+    u0 = scale_cols(sine_derivs(O.nodes(0.0, h, n, True, O.PRIMAL), M, 0.0), h)
+    rng = np.random.default_rng(3)
+    runs = []
+    for uu in (u0, u0 * (1.0 + 2.2e-16 * rng.standard_normal(u0.shape))):
+        a, b, par = uu, np.zeros((n, M)), O.PRIMAL
+        for _ in range(nhalf):
+            a, b = O.half_step_1d(a, b, par, n, True, 0.0, h, M, LAM)
+            par = O.flip(par)
+        runs.append((a, b))
+    for i, (got, want) in enumerate(((pair.u.values.cpu().numpy(), g["n200/u"]),
+                                     (pair.v.values.cpu().numpy(), g["n200/v"]))):
+        sigma = float(np.max(np.abs(runs[1][i] - runs[0][i])))
+        scale = float(np.max(np.abs(want)))
+        assert float(np.max(np.abs(got - want))) <= max(2e-12 * scale, 10.0 * sigma)
+    # at n_x = 200 both runs sit at the rounding floor (~1e-13): same order of magnitude
+    assert np.all(e < 1e-12) and np.all(e < 3.0 * g["n200/errors"]) and np.all(g["n200/errors"] < 3.0 * e)
