@@ -410,6 +410,7 @@ def main():
                                             f"of hermwave.half_step_2d)"}
     if rank == 0 and world == 1 and not args.no_c3:
         result["c3"] = c3_bench(hb, torch, pk)
+        result["c5"] = c5_bench(hb, torch, pk)
     if rank == 0 and world == 1 and not args.no_sweep:
         result["sweep"] = sweep(hb, torch, pk)
     if rank == 0:
@@ -488,9 +489,55 @@ def c3_bench(hb, torch, pk):
     g = cells * dof_per_node(m, "cons") / sec / 1e9
     tf = f_alg_cons(m) * cells / sec / 1e12
     del par
+    # the conservation check (no 2D energy exists in the reference):
+    # the two-level update is exactly reversible, so N steps forward, swap the
+    # levels, N steps back must return the start (App. A.7)
+    st0 = {"a": state["a"].clone(), "b": state["b"].clone(), "pa": state["pa"]}
+    nrev = 20
+    for i in range(nrev):
+        one(i)
+    state["a"], state["b"] = state["b"], state["a"]
+    state["pa"] = hb.flip(state["pa"])
+    for i in range(nrev):
+        one(i)
+    # back at the start with the levels swapped: current <-> previous
+    rev = max(float((state["b"] - st0["a"]).abs().max()) / float(st0["a"].abs().max()),
+              float((state["a"] - st0["b"]).abs().max()) / float(st0["b"].abs().max()))
     return {"workload": "2D conservative Hermite m=5, 2048^2, Dirichlet x / Neumann y walls (C3)",
             "gdof_per_s": g, "ms_per_step": sec * 1e3, "tflops_falg": tf, "frac_dmma_peak": tf / pk["dmma_tflops"],
-            "hbm_gbs": 24 * cells * dof_per_node(m, "cons") / sec / 1e9}
+            "hbm_gbs": 24 * cells * dof_per_node(m, "cons") / sec / 1e9,
+            "conservation_check": {"kind": f"time reversal: {nrev} steps forward, levels swapped, {nrev} back",
+                                   "max_rel_deviation": rev}}
+
+
+def c5_bench(hb, torch, pk):
+    """Config C5 at its single-GPU size: dissipative m = 6 on 8192^2 (45.6 GB
+    per level), the strong-scaling base of the 1/2/4/8-GPU runs."""
+    from paper_1802_05246_b200.stepping import diss2d_into
+
+    m, n = 6, 8192
+    grid = hb.Grid2D(0.0, 1.0, 0.0, 1.0, n, n, True)
+    cfg = hb.SchemeConfig(m=m, lam=0.9)
+    w = 2.0 * math.pi
+    u = hb.standing_wave_on_grid(grid, hb.PRIMAL, 0.1, m, m, w, w, w * math.sqrt(2.0))
+    v = hb.standing_wave_on_grid(grid, hb.PRIMAL, 0.1, m - 1, m - 1, w, w, w * math.sqrt(2.0), tder=1)
+    bufs = [(u, v), (torch.empty_like(u), torch.empty_like(v))]
+    st = {"par": hb.PRIMAL}
+
+    def one(i):
+        diss2d_into(*bufs[i % 2], *bufs[(i + 1) % 2], grid, st["par"], m, cfg, hb.BoundarySpec2D())
+        st["par"] = hb.flip(st["par"])
+
+    for i in range(2):
+        one(i)
+    torch.cuda.synchronize()
+    sec = _time_steps(torch, lambda i: one(i + 2), 4)
+    tf = f_alg_diss(m) * n * n / sec / 1e12
+    del u, v, bufs
+    torch.cuda.empty_cache()
+    return {"workload": "2D periodic dissipative Hermite m=6, 8192^2 (C5 single-GPU size)",
+            "gdof_per_s": n * n * dof_per_node(m) / sec / 1e9, "ms_per_step": sec * 1e3, "tflops_falg": tf,
+            "frac_dmma_peak": tf / pk["dmma_tflops"]}
 
 
 def sweep(hb, torch, pk):
