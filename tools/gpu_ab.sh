@@ -9,7 +9,7 @@ CONFIGS=${AB_CONFIGS:-"diss:2:1024 diss:3:1024 diss:4:1024 diss:5:1024 diss:6:10
 # parity of each variant first (a broken variant's timing means nothing)
 for v in "$@"; do
   if [ "$v" = default ]; then lib=""; else lib=build_var/$v/libhermb200.so; fi
-  echo "parity [$v]: $(HERMB200_LIB=$lib timeout 300 python -m pytest tests/test_gpu_parity.py tests/test_gpu_slab.py -q -x 2>&1 | tail -1)" >> $out
+  echo "parity [$v]: $(HERMB200_LIB=$lib timeout 400 python -m pytest tests/test_gpu_parity.py tests/test_gpu_slab.py tests/test_gpu_interior.py -q -x 2>&1 | tail -1)" >> $out
 done
 for round in 1 2; do
   for v in "$@"; do
