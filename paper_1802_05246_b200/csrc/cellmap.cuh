@@ -45,6 +45,16 @@ struct CellMapArgs {
   double gxl, gxh, gyl, gyh;   // Dirichlet data, field 0 only
 };
 
+// L2 prefetch size qualifier of the staging copies (A/B knob HW_CM_PFN = 64 / 128 / 256)
+#if defined(HW_CM_PFN) && HW_CM_PFN == 64
+#define HW_CM_PF ".L2::64B"
+#elif defined(HW_CM_PFN) && HW_CM_PFN == 128
+#define HW_CM_PF ".L2::128B"
+#elif defined(HW_CM_PFN) && HW_CM_PFN == 256
+#define HW_CM_PF ".L2::256B"
+#else
+#define HW_CM_PF ""
+#endif
 #ifndef HW_CM_SLEEP
 #define HW_CM_SLEEP 64  // producer back-off (ns) while its ring slot is busy and no slab is ready
 #endif
@@ -169,10 +179,10 @@ struct CMCfg {
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void cm_cp_async8(double* dst, const double* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+  asm volatile("cp.async.ca.shared.global" HW_CM_PF " [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cm_cp_async16(double* dst, const double* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+  asm volatile("cp.async.cg.shared.global" HW_CM_PF " [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 
 // mbarrier primitives (CTA scope).
