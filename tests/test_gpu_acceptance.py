@@ -1,0 +1,62 @@
+"""The reference's long-horizon acceptance criteria on the device
+(test_acceptance.py:107-135 criterion 4, :262-297 criterion 7): 10^4
+conservative steps keep the exact 1D energy to 1e-8 (smooth data, and below
+random data's drift), 10^4 dissipative half steps stay bounded by twice the
+initial sup norm.  Same configurations and thresholds as the reference."""
+
+import math
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _drift(m, mode, steps=10_000, lam=0.5, n0=30, seed=123):
+    from paper_1802_05246_b200 import studies as S
+
+    cfg = replace(S.default_config("conserve1d"), m=m, mode=mode, steps=steps, lam=lam, n0=n0, seed=seed).validate()
+    _, _, deltas, e0 = S.run_conservation_1d(cfg)
+    return float(np.max(np.abs(deltas)) / e0)
+
+
+@pytest.mark.parametrize("m", [1, 3])
+def test_criterion4_smooth_energy_drift(m):
+    assert _drift(m, "smooth") <= 1e-8
+
+
+def test_criterion4_smooth_below_random():
+    assert _drift(1, "smooth") < _drift(1, "random")
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4])
+def test_criterion7_conservative_long_run(m):
+    assert _drift(m, "smooth", lam=1.0, n0=10) <= 1e-8
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4])
+def test_criterion7_dissipative_long_run(m):
+    import torch
+
+    import paper_1802_05246_b200 as hb
+
+    n = 10
+    grid = hb.Grid1D(-math.pi, math.pi, n, True)
+    cfg = hb.SchemeConfig(m=m, lam=1.0)
+    bc = hb.BoundarySpec()
+    xs = grid.nodes(hb.PRIMAL)
+    h = grid.h
+    u = np.stack([np.sin(xs + l * math.pi / 2) * h**l / math.factorial(l) for l in range(m + 1)], axis=-1)
+    v = np.stack([-np.cos(xs + l * math.pi / 2) * h**l / math.factorial(l) for l in range(m)], axis=-1)
+    pair = hb.FieldPair(hb.Field1D(grid, hb.PRIMAL, 0.0, torch.from_numpy(u).cuda()),
+                        hb.Field1D(grid, hb.PRIMAL, 0.0, torch.from_numpy(v).cuda()))
+    sup0 = float(np.abs(u[:, 0]).max())
+    sup = sup0
+    for k in range(10_000):
+        pair = hb.half_step_1d(pair, cfg, bc)
+        if (k + 1) % 100 == 0:
+            vals = pair.u.values.cpu().numpy()
+            assert np.all(np.isfinite(vals))
+            sup = max(sup, float(np.abs(vals[:, 0]).max()))
+    assert sup <= 2.0 * sup0
