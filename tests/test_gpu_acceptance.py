@@ -92,3 +92,80 @@ def test_criteria_1_to_3_rates_match_reference(acc_gold, exp, scheme, m, lam):
     np.testing.assert_array_equal(rep.ns, acc_gold[f"{k}/ns"])
     np.testing.assert_allclose(rep.err_u, acc_gold[f"{k}/err_u"], rtol=1e-9, atol=1e-15)
     assert rep.rate() == pytest.approx(float(acc_gold[f"{k}/rate"]), abs=1e-6)
+
+
+# criterion 5 (test_acceptance.py:141-203): one step is exact for the cell
+# interpolant — the d'Alembert centre value of the interpolated pair, and the
+# conservative average of the interpolant at +-rho h — to 1e-12.
+@pytest.mark.parametrize("m", [1, 2, 3, 4])
+@pytest.mark.parametrize("lam", [0.5, 1.0])
+def test_criterion5_dissipative_polynomial_exactness(m, lam):
+    from numpy.polynomial import Polynomial as Poly
+
+    import paper_1802_05246_b200 as hb
+    from oracle import hermite_oracle as O
+
+    rng = np.random.default_rng(500 + m)
+    n = 6
+    grid = hb.Grid1D(0.0, 3.0, n, True)
+    u = rng.standard_normal((n, m + 1))
+    v = rng.standard_normal((n, m))
+    out = hb.half_step_1d(hb.FieldPair(hb.Field1D(grid, hb.PRIMAL, 0.0, u), hb.Field1D(grid, hb.PRIMAL, 0.0, v)),
+                          hb.SchemeConfig(m=m, lam=lam), hb.BoundarySpec())
+    ud = O.pair_data(u, O.PRIMAL, True, O.PERIODIC_BC)
+    vd = O.pair_data(v, O.PRIMAL, True, O.PERIODIC_BC)
+    scale = np.abs(ud).max()
+    h, s0 = grid.h, 0.5 * lam
+    worst = 0.0
+    for i in range(n):
+        pu, pv = Poly(O.interp_1d(ud[i])), Poly(O.interp_1d(vd[i]))
+        qint, dp = pv.integ(), pu.deriv()
+        uref = 0.5 * (pu(s0) + pu(-s0)) + (h / 2.0) * (qint(s0) - qint(-s0))
+        vref = (1.0 / (2 * h)) * (dp(s0) - dp(-s0)) + 0.5 * (pv(s0) + pv(-s0))
+        worst = max(worst, abs(out.u.values[i, 0] - uref) / scale, abs(out.v.values[i, 0] - vref) / scale)
+    assert worst <= 1e-12
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4])
+@pytest.mark.parametrize("lam", [0.5, 1.0])
+def test_criterion5_conservative_polynomial_exactness(m, lam):
+    from numpy.polynomial import Polynomial as Poly
+
+    import paper_1802_05246_b200 as hb
+    from oracle import hermite_oracle as O
+
+    rng = np.random.default_rng(520 + m)
+    n = 6
+    grid = hb.Grid1D(0.0, 3.0, n, True)
+    cur = rng.standard_normal((n, m + 1))
+    prev = rng.standard_normal((n, m + 1))
+    out = hb.full_step_conservative(hb.TwoLevelState(hb.Field1D(grid, hb.PRIMAL, 0.0, cur),
+                                                     hb.Field1D(grid, hb.DUAL, -0.1, prev)),
+                                    hb.SchemeConfig(m=m, lam=lam), hb.BoundarySpec())
+    coeffs = O.interp_1d(O.pair_data(cur, O.PRIMAL, True, O.PERIODIC_BC))
+    scale = np.abs(coeffs).max()
+    rho = 0.5 * lam
+    worst = 0.0
+    for i in range(n):
+        p = Poly(coeffs[i])  # in the cell's scaled variable (x - centre) / h
+        ref = 2.0 * (0.5 * (p(rho) + p(-rho))) - prev[i, 0]
+        worst = max(worst, abs(out.current.values[i, 0] - ref) / scale)
+    assert worst <= 1e-12
+
+
+# criterion 8 (test_acceptance.py:298-322): reflections are involutions, and a
+# Dirichlet (Neumann) wall suppresses the even (odd) interpolant coefficients.
+@pytest.mark.parametrize("m", [1, 2, 3, 4])
+def test_criterion8_reflections(m):
+    import paper_1802_05246_b200 as hb
+
+    rng = np.random.default_rng(800 + m)
+    data = rng.standard_normal((6, m + 1))
+    for kind in ("dirichlet0", "neumann0"):
+        assert np.array_equal(hb.ghost_data(hb.ghost_data(data, kind), kind), data)
+    b = np.random.default_rng(810 + m).standard_normal(m + 1)
+    scale = np.abs(b).max()
+    even = hb.apply_interp(np.stack([hb.ghost_data(b[None], "dirichlet0")[0], b]))
+    odd = hb.apply_interp(np.stack([hb.ghost_data(b[None], "neumann0")[0], b]))
+    assert np.abs(even[0::2]).max() / scale <= 1e-13
+    assert np.abs(odd[1::2]).max() / scale <= 1e-13
