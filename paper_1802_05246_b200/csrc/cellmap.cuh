@@ -157,6 +157,16 @@ struct CMCfg {
   static constexpr unsigned WIDE = wide_mask();
 #endif
   static constexpr int SLAB = DIRECT ? 0 : MT * NT * 64;
+  // The fragment-order slab rotates n-tile nt's 32 lane slots by SWZ * nt:
+  // the drain's record-order gather then spreads a cell's outputs of equal
+  // column over more banks (the consumer's 16-byte stores stay conflict-free).
+  // Measured 1.5-4% faster for every order except conservative m = 3 (+4%).
+  static constexpr int SWZ0 = (SCH == kCons && M == 3) ? 0 : 1;
+#ifdef HW_CM_SWZ
+  static constexpr int SWZ = cm_knob(SCH, M) ? HW_CM_SWZ : SWZ0;
+#else
+  static constexpr int SWZ = SWZ0;
+#endif
   static constexpr int PSLAB = SCH == kCons ? MT * 8 * O0 : 0;
   static constexpr int TAIL = tail(MT);
 #ifdef HW_CM_NS
@@ -319,7 +329,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
     const int o = code & 0xffff;
     for (int r = 0; r < 8; ++r) {
       const int q = (code >> 16) ? 8 * C::O0 + r * C::O1 + o : r * C::O0 + o;
-      s_inv[q] = (nt * 32 + r * 4 + col / 2) * 2 + col % 2;
+      s_inv[q] = (nt * 32 + ((r * 4 + col / 2 + C::SWZ * nt) & 31)) * 2 + col % 2;
     }
   }
   if (tid == 0) {
@@ -760,7 +770,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       for (int t = 0; t < MT; ++t)
 #pragma unroll
         for (int n = 0; n < NT; ++n)
-          *reinterpret_cast<double2*>(slab + t * NT * 64 + (n * 32 + lane) * 2) =
+          *reinterpret_cast<double2*>(slab + t * NT * 64 + (n * 32 + ((lane + C::SWZ * n) & 31)) * 2) =
               make_double2(acc[t][n][0], acc[t][n][1]);
       if (SCH == kCons) asm volatile("cp.async.wait_all;\n" ::: "memory");  // `previous` landed
       __syncwarp();
