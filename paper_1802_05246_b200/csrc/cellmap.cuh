@@ -13,12 +13,20 @@
 //
 // Warp specialisation.  Four producer warps stage, for every (tile, K-chunk)
 // of the CTA's persistent tile sequence, the 16-entry slices of the tile's
-// (TR+1) x (TJ+1) source nodes plus the chunk's W fragments into an NS-deep
-// shared-memory ring with cp.async; completion is tracked by mbarriers
-// (cp.async.mbarrier.arrive), never by a CTA-wide barrier.  Eight consumer
-// warps wait on the ring's `full` barriers, run the DMMAs and release the slot
-// on its `empty` barrier, so consumers drift freely relative to each other and
-// the epilogue of one warp overlaps the tensor-core work of the others.
+// (TR+1) x (TJ+1) source nodes (plus the chunk's W fragments unless W is
+// resident) into an NS-deep shared-memory ring with cp.async; completion is
+// tracked by mbarriers (cp.async.mbarrier.arrive), never by a CTA-wide
+// barrier.  Eight or twelve consumer warps wait on the ring's `full`
+// barriers, run the DMMAs and release the slot on its `empty` barrier, so
+// consumers drift freely relative to each other.  Each consumer dumps its
+// accumulators into its own output slab and moves on; a producer warp drains
+// the slab to HBM between staging steps (or, per order, the consumer stores
+// directly / drains its own slab).
+//
+// Every per-order choice (consumer warps, M-tiles per warp, tile width, ring
+// depth, resident W, epilogue kind, ...) lives in CMCfg / cellmap_shape.h with
+// the measurement that picked it; profiles/ab_r01_kernel_knobs.txt has the
+// A/B tables (tools/gpu_ab.sh, variant builds via -DHW_CM_* knobs).
 #pragma once
 
 #include <stdint.h>
