@@ -118,11 +118,6 @@ struct CMCfg {
   static constexpr bool DIRECT = cm_direct(SCH, M);
   static constexpr bool SELF = cm_self(SCH, M) && !DIRECT;
   static constexpr bool OWN = DIRECT || SELF;  // the consumers write HBM themselves
-#ifdef HW_CM_XCHUNK
-  static constexpr bool XCHUNK = HW_CM_XCHUNK;
-#else
-  static constexpr bool XCHUNK = false;  // cross-chunk operand prefetch (A/B knob)
-#endif
   static constexpr int tail(int mt) {
     return WRESN * 8 + NW * ((DIRECT ? 0 : mt * NT * 64) + (SCH == kCons ? mt * 8 * O0 : 0)) * 8 + (8 * DO + 8 * NT) * 4 +
            (2 * NSMAX + 2 * NW) * 8 + 64;
@@ -647,13 +642,6 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
   int tile = blockIdx.x, ch = 0, k = 0;  // k = this warp's tile count
   CMTile cg = tile_geo(tile);
   double* slab = slabs + warp * C::SLAB;
-  // k-step operand registers, double-buffered across the whole stage sequence:
-  // raw[.][r] = the two y-corners of staged row trl0 + r (row r + 1 of
-  // M-tile r is row 0 of M-tile r + 1: MT + 1 rows feed MT M-tiles)
-  double raw[2][MT + 1][2];
-  double bb[C::PREFETCH_B ? 2 : 1][NT];
-  bool pre = false;
-  int off = 0;
   for (int g = 0; g < nstages; ++g) {
     const int b = g % NS;
     if (ch == NCH - 1) {
@@ -673,32 +661,24 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
         }
       }
     }
-    // XCHUNK: the first k-step operands of the coming chunk were loaded under
-    // the previous chunk's last DMMAs (cross-chunk prefetch); `pre` says so and
-    // `off` is the register-buffer parity they sit in.
-    if (!pre) mbar_wait(&full[b], (g / NS) & 1);
+    mbar_wait(&full[b], (g / NS) & 1);
     const double* cb = smem + b * C::SBUF;
     const double* wb = C::WRES ? smem + C::WRES0 + ch * KSC * NT * 32 : cb + C::CBUF;
-    // the chunk after this one (for the prefetch)
-    const int chn = ch + 1 == NCH ? 0 : ch + 1;
-    const bool has_next = C::XCHUNK && g + 1 < nstages;
-    const int bn = (g + 1) % NS;
-    const double* cbn = smem + bn * C::SBUF;
-    const double* wbn = C::WRES ? smem + C::WRES0 + chn * KSC * NT * 32 : cbn + C::CBUF;
     // One chunk of NKS k-steps, software-pipelined: the shared-memory
     // operands of k-step ks+1 (corner values; W fragments when registers
     // allow) are loaded before the DMMAs of k-step ks issue.  FIRST: the
     // tile's first chunk, whose first k-step starts the accumulators (C = 0).
-    // OFF: register-buffer parity of k-step 0.
-    auto run_chunk = [&](auto nks_c, auto first_c, auto off_c) {
+    auto run_chunk = [&](auto nks_c, auto first_c) {
       constexpr int NKS = decltype(nks_c)::value;
       constexpr bool FIRST = decltype(first_c)::value;
-      constexpr int OFF = decltype(off_c)::value;
       constexpr bool PREB = C::PREFETCH_B;
+      // raw[.][r] = the two y-corners of staged row trl0 + r (row r + 1 of
+      // M-tile r is row 0 of M-tile r + 1: MT + 1 rows feed MT M-tiles)
+      double raw[2][MT + 1][2];
+      double bb[PREB ? 2 : 1][NT];
       const int trl0 = (warp / (TJ / 8)) * MT, tc = (warp % (TJ / 8)) * 8;
-      const int node0 = (trl0 * (TJ + 1) + tc + (lane >> 2)) * KCP + (lane & 3);
-      auto load_from = [&](const double* cbx, const double* wbx, const int ks, const int slot) {
-        const double* pbase = cbx + node0;
+      const double* pbase = cb + (trl0 * (TJ + 1) + tc + (lane >> 2)) * KCP + (lane & 3);
+      auto load = [&](const int ks, const int slot) {
 #pragma unroll
         for (int r = 0; r <= MT; ++r) {
           const double* p = pbase + r * (TJ + 1) * KCP + ks * 4;
@@ -706,16 +686,16 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
           raw[slot][r][1] = p[KCP];
         }
         if (PREB) {
-          const double* wk = wbx + ks * NT * 32 + lane;
+          const double* wk = wb + ks * NT * 32 + lane;
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) bb[PREB ? slot : 0][nt] = wk[nt * 32];
         }
       };
-      if (!pre) load_from(cb, wb, 0, OFF);
+      load(0, 0);
 #pragma unroll
       for (int ks = 0; ks < NKS; ++ks) {
-        const int cur = (ks + OFF) & 1;
-        if (ks + 1 < NKS) load_from(cb, wb, ks + 1, cur ^ 1);
+        const int cur = ks & 1;
+        if (ks + 1 < NKS) load(ks + 1, cur ^ 1);
         const int step = ch * KSC + ks;
         const unsigned long long mx = ((kxbits >> step) & 1ull) << 63;
         const unsigned long long my = ((kybits >> step) & 1ull) << 63;
@@ -745,39 +725,21 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
               dmma(acc[t][nt], A[t][c], bf);
           }
         }
-        if (ks + 1 == NKS && has_next) {  // under the last DMMAs: the next chunk's first operands
-          mbar_wait(&full[bn], ((g + 1) / NS) & 1);
-          load_from(cbn, wbn, 0, cur ^ 1);
-        }
       }
     };
     if constexpr (MODE != 2) {
       using KF = std::integral_constant<int, KSC>;
       using KL = std::integral_constant<int, C::NK - (NCH - 1) * KSC>;
-      using O0 = std::integral_constant<int, 0>;
-      using O1 = std::integral_constant<int, 1>;
-      auto dispatch = [&](auto off_c) {
-        if constexpr (NCH == 1) {
-          run_chunk(KL{}, std::true_type{}, off_c);
-        } else {
-          if (ch == 0)
-            run_chunk(KF{}, std::true_type{}, off_c);
-          else if (ch == NCH - 1)
-            run_chunk(KL{}, std::false_type{}, off_c);
-          else
-            run_chunk(KF{}, std::false_type{}, off_c);
-        }
-      };
-      if (off == 0)
-        dispatch(O0{});
-      else
-        dispatch(O1{});
-    }
-    // parity of the next chunk's first k-step, and whether it is loaded
-    {
-      const int nks = ch == NCH - 1 ? C::NK - (NCH - 1) * KSC : KSC;
-      off = (off + nks) & 1;
-      pre = has_next && MODE != 2;
+      if constexpr (NCH == 1) {
+        run_chunk(KL{}, std::true_type{});
+      } else {
+        if (ch == 0)
+          run_chunk(KF{}, std::true_type{});
+        else if (ch == NCH - 1)
+          run_chunk(KL{}, std::false_type{});
+        else
+          run_chunk(KF{}, std::false_type{});
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[b]);  // ring slot b may be refilled
