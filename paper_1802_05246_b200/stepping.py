@@ -94,7 +94,9 @@ def _diss2d_host_pipelined(uh, vh, grid, parity, m, cfg: SchemeConfig, bc: Bound
     s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     s_in.wait_stream(comp)
     off = 0 if parity == PRIMAL else -1
-    edges = np.linspace(0, nsrc, nchunks + 1).astype(int)
+    # chunk boundaries: nchunks equal chunks, or explicit fractions of the rows
+    fr = np.linspace(0.0, 1.0, nchunks + 1) if np.isscalar(nchunks) else np.asarray(nchunks, dtype=float)
+    edges = np.unique(np.round(fr * nsrc).astype(int))
     ranges = list(zip(edges[:-1], edges[1:]))
     if off == 0:
         # from primal data a target chunk also reads the first row of the next
@@ -122,7 +124,7 @@ def _diss2d_host_pipelined(uh, vh, grid, parity, m, cfg: SchemeConfig, bc: Bound
 
     dt = cfg.dt(min(grid.hx, grid.hy))
     cap = -1 if cfg.stage_cap is None else int(cfg.stage_cap)
-    tedges = np.linspace(0, ntx, nchunks + 1).astype(int)
+    tedges = np.unique(np.round(fr * ntx).astype(int))
     for t0, t1 in zip(tedges[:-1], tedges[1:]):
         if t1 <= t0:
             continue

@@ -26,7 +26,9 @@ def main():
     hu.copy_(u)
     hv.copy_(v)
     dof = n * n * ((m + 1) ** 2 + m * m)
-    for nch in (8, 16, 24, 32, 48):
+    geo = lambda *f: [0.0, *f, 1.0]  # noqa: E731
+    for nch in (8, 16, geo(0.02, 0.1, 0.25, 0.45, 0.65, 0.85, 0.96), geo(0.015, 0.06, 0.2, 0.4, 0.6, 0.8, 0.92, 0.98),
+                geo(0.03, 0.2, 0.4, 0.6, 0.8, 0.97), geo(0.01, 0.05, 0.15, 0.35, 0.55, 0.75, 0.9, 0.97, 0.99)):
         a, b, par = hu.numpy(), hv.numpy(), hb.PRIMAL
         ts = []
         for i in range(8):
@@ -37,7 +39,7 @@ def main():
             ts.append(time.perf_counter() - t0)
             par = hb.flip(par)
         best = sorted(ts[2:])
-        print(f"nchunks={nch}: median {1e3 * best[len(best) // 2]:.2f} ms, best {1e3 * best[0]:.2f} ms "
+        print(f"chunks={nch if isinstance(nch, int) else len(nch) - 1}: median {1e3 * best[len(best) // 2]:.2f} ms, best {1e3 * best[0]:.2f} ms "
               f"-> {dof / best[len(best) // 2] / 1e9:.2f} GDOF/s")
 
 
