@@ -73,7 +73,7 @@ typedef struct {
 
 /* Library info. */
 const char* hw_last_error(void);
-int hw_version(void);
+int hw_version(void);              /* 3: + 2D seminorm, lower-level batched API */
 int hw_max_order(void);            /* largest m with a compiled fast path */
 
 /* interp.py:51-75 interp_matrix(mu): (2mu+2)^2 row-major, exact doubles. */

@@ -250,7 +250,7 @@ using namespace hw;
 extern "C" {
 
 const char* hw_last_error(void) { return g_err.c_str(); }
-int hw_version(void) { return 2; }
+int hw_version(void) { return 3; }
 int hw_max_order(void) { return kMaxFast; }
 
 int hw_interp_matrix(int mu, double* out) {
