@@ -179,14 +179,14 @@ struct CMCfg {
   static constexpr int TAIL = tail(MT);
 #ifdef HW_CM_NS
   static constexpr int NS = cm_knob(SCH, M) && fits(MT, HW_CM_NS) ? HW_CM_NS :
-      ((SCH != kDiss && M == 4) ? 3 : (fits_soft(MT, 4) ? 4 : (fits(MT, 3) ? 3 : 2)));
+      (M == 4 ? 3 : (fits_soft(MT, 4) ? 4 : (fits(MT, 3) ? 3 : 2)));
 #elif defined(HW_CM_NSDEEP)
   // deepest ring within the soft limit (at least 2)
   static constexpr int deepest(int ns) { return ns <= 2 ? 2 : (fits_soft(MT, ns) ? ns : deepest(ns - 1)); }
   static constexpr int NS = deepest(NSMAX);
 #else
-  // (conservative m = 4: 3 slots measured 5% faster than 4, tools/gpu_ab.sh)
-  static constexpr int NS = (SCH != kDiss && M == 4) ? 3 : (fits_soft(MT, 4) ? 4 : (fits(MT, 3) ? 3 : 2));
+  // (m = 4: 3 slots measured faster than 4 — conservative 5%, dissipative 0.5-0.8%; tools/gpu_ab.sh)
+  static constexpr int NS = M == 4 ? 3 : (fits_soft(MT, 4) ? 4 : (fits(MT, 3) ? 3 : 2));
 #endif
   static constexpr int WRES0 = NS * SBUF;          // double offset of the resident W
   static constexpr int EPI0 = WRES0 + WRESN;       // double offset of the slabs
