@@ -63,6 +63,9 @@ struct CellMapArgs {
 #else
 #define HW_CM_PF ""
 #endif
+#ifndef HW_CM_PDL
+#define HW_CM_PDL 1  // programmatic dependent launch between consecutive steps (A/B knob)
+#endif
 #ifndef HW_CM_SLEEP
 #define HW_CM_SLEEP 64  // producer back-off (ns) while its ring slot is busy and no slab is ready
 #endif
@@ -351,6 +354,16 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
     }
   }
   __syncthreads();
+#if HW_CM_PDL
+  // Programmatic dependent launch (cellmap_launch.cuh): the setup above ran
+  // while the previous step's grid was still finishing; every read of step
+  // data and every output store comes after this wait, which returns once
+  // that grid has completed and its stores are visible.  Then let the next
+  // step's grid be scheduled, so its CTAs take each SM as this grid's CTA
+  // there exits and run their setup under this grid's tail.
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+#endif
 
   const int tcols = (int)((a.nty + TJ - 1) / TJ);
   const int ntiles = tcols * (int)((a.ntrows + TR - 1) / TR);

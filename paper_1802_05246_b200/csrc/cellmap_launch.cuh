@@ -45,8 +45,25 @@ cudaError_t launch_cellmap(const CellMapArgs& a, cudaStream_t st) {
   int64_t nblk = cached - 1;
   if (nblk > ntiles) nblk = ntiles;
   if (nblk <= 0) return cudaSuccess;
+#if HW_CM_PDL
+  // Programmatic stream serialisation: this grid may be scheduled before the
+  // previous kernel in the stream has finished; the kernel's
+  // griddepcontrol.wait holds every access to step data until it has.
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)nblk);
+  lc.blockDim = dim3(C::NTHREADS);
+  lc.dynamicSmemBytes = C::SMEM;
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  return cudaLaunchKernelEx(&lc, kern, a);
+#else
   kern<<<(unsigned)nblk, C::NTHREADS, C::SMEM, st>>>(a);
   return cudaGetLastError();
+#endif
 }
 
 #define HW_INSTANTIATE_CELLMAP(M)                                                   \
