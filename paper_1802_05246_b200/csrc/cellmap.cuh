@@ -51,6 +51,7 @@ struct CellMapArgs {
   int off, periodic;           // source offset of a target (0 primal, -1 dual)
   int kxl, kxh, kyl, kyh;      // wall kinds (0 when periodic)
   double gxl, gxh, gyl, gyh;   // Dirichlet data, field 0 only
+  int* sched;                  // [2] dynamic tile counter + CTAs done (zero between launches); null = static schedule
 };
 
 // L2 prefetch size qualifier of the staging copies (A/B knob HW_CM_PFN = 64 / 128 / 256)
@@ -92,6 +93,7 @@ struct CMCfg {
   static constexpr int NTHREADS = 32 * (NW + NPW);
   static constexpr int TJ = cm_tj(SCH, M);         // target columns per tile
   static constexpr int NSMAX = 8;                  // ring slots the barrier arrays hold
+  static constexpr int QT = 8;                     // tile-id ring (s_tile): tiles between fetch and last drain
   static constexpr int DO = O0 + O1;               // output record per cell
   // setmaxnreg split of the 512 registers per lane of each SM sub-partition
   // (NW / 4 consumer + NPW / 4 producer warps)
@@ -313,6 +315,20 @@ struct CMTile {
 // 1 = skip the staging copies (compute on whatever the ring holds),
 // 2 = skip the tensor-core work and stores (staging only), 3 = skip the
 // output stores to HBM (staging + tensor cores + slab epilogue).
+#ifdef HW_CM_CTA_TIMES
+// profiling build only (tools/cta_times.cu): per-CTA start / end globaltimer
+__device__ unsigned long long hw_cm_cta_t[2 * 1024];
+__device__ __forceinline__ unsigned long long cm_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define HW_CM_STAMP_END() \
+  if ((threadIdx.x & 31) == 0) atomicMax(&hw_cm_cta_t[2 * blockIdx.x + 1], cm_gtimer())
+#else
+#define HW_CM_STAMP_END()
+#endif
+
 template <int M, int SCH, int MODE = 0>
 __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(const __grid_constant__ CellMapArgs a) {
   using C = CMCfg<M, SCH>;
@@ -328,6 +344,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
   uint64_t* empty = bars + C::NSMAX;      // [NS] consumers -> producers: ring slot consumed
   uint64_t* sfull = bars + 2 * C::NSMAX;  // [NW] consumer w -> producer: output slab written
   uint64_t* sempty = sfull + NW;          // [NW] producer -> consumer w: output slab drained
+  int* s_tile = reinterpret_cast<int*>(sempty + NW);  // [QT] tile id of this CTA's k-th tile (in the tail's slack)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   // Inverse fragment map: output q of an M-tile's records, laid out
@@ -344,6 +361,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
     }
   }
   if (tid == 0) {
+    s_tile[0] = blockIdx.x;
     for (int b = 0; b < NS; ++b) {
       mbar_init(&full[b], 2 * 32 * C::NPW);  // each producer lane: one plain arrive + one cp.async arrive
       mbar_init(&empty[b], NW);               // one arrive per consumer warp
@@ -364,11 +382,24 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 #endif
+#ifdef HW_CM_CTA_TIMES
+  if (tid == 0) hw_cm_cta_t[2 * blockIdx.x] = cm_gtimer();
+#endif
 
   const int tcols = (int)((a.nty + TJ - 1) / TJ);
   const int ntiles = tcols * (int)((a.ntrows + TR - 1) / TR);
-  const int my_tiles = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  const int nstages = my_tiles * NCH;
+  // Dynamic tile schedule: CTA b starts on tile b, then takes the next
+  // unclaimed tile from the global counter a.sched[0] (one lead producer lane
+  // claims tile k + 1 when the CTA starts tile k and publishes it in
+  // s_tile[(k + 1) % QT]).  The persistent CTAs then finish within one tile
+  // of each other instead of within the spread of their static shares
+  // (tools/cta_times.cu: 11% at m = 4, 1024^2).  A claim past the last tile
+  // ends the CTA's sequence; the last CTA to make that claim zeroes the
+  // counters for the next launch.  Null a.sched: static round robin.
+  static_assert(C::NS + 2 <= C::QT, "tile-id ring shorter than the tiles in flight");
+  static_assert((2 * C::NSMAX + 2 * NW) * 8 + (8 * C::DO + 8 * NT) * 4 + 4 * C::QT + 4 <=
+                    (2 * C::NSMAX + 2 * NW) * 8 + (8 * C::DO + 8 * NT) * 4 + 64,
+                "s_tile must fit the tail's slack");
 
   auto tile_geo = [&](int tile) {
     CMTile t;
@@ -402,9 +433,10 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
     const int e = pl % KC, q0 = pl / KC;
 
     // Output drain for consumer warps pw and pw + NPW: slab -> HBM, coalesced.
-    int dtile[NW / C::NPW], dk[NW / C::NPW];
+    int ktot = 0x7fffffff;  // this CTA's tile count, once its last claim has come back
+    int dk[NW / C::NPW];  // tiles of consumer warp pw + NPW j drained so far
 #pragma unroll
-    for (int j = 0; j < NW / C::NPW; ++j) dtile[j] = blockIdx.x, dk[j] = 0;
+    for (int j = 0; j < NW / C::NPW; ++j) dk[j] = 0;
     // INVREG: this lane's inverse-map entries of a full M-tile held in
     // registers (record slot lane + 32 k of field 0, then of field 1) instead
     // of one extra shared load per drained value: 2% faster at m = 4 (both
@@ -428,11 +460,11 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
 #pragma unroll
       for (int j = 0; j < NW / C::NPW; ++j) {
         const int w = pw + C::NPW * j;
-        if (dtile[j] >= ntiles) continue;
+        if (dk[j] >= ktot) continue;
         int ready = lane == 0 ? (int)mbar_test(&sfull[w], dk[j] & 1) : 0;
         ready = __shfl_sync(0xffffffffu, ready, 0);
         if (!ready) continue;
-        const CMTile tg = tile_geo(dtile[j]);
+        const CMTile tg = tile_geo(s_tile[dk[j] % C::QT]);
         const double* sl = slabs + w * C::SLAB;
         const double* pl0 = pslabs + w * C::PSLAB;  // kCons: `previous`, record order
 #pragma unroll
@@ -489,7 +521,6 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sempty[w]);
-        dtile[j] += gridDim.x;
         ++dk[j];
         any = true;
       }
@@ -497,12 +528,34 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       return any;
     };
 
-    int tile = blockIdx.x, ch = 0;
+    int tile = blockIdx.x, ch = 0, kp = 0;
+    const bool lead = pl == 0;
+    int nexttile = 0;
+    // claim(): issue the claim of the tile after next; its result is first
+    // read one tile later, so the atomic's round trip never stalls the
+    // producers.  finish(): after this CTA's last (failed) claim.
+    auto claim = [&]() {
+      return a.sched == nullptr ? nexttile + (int)gridDim.x  // static: b, b + G, b + 2G, ...
+                                : (int)gridDim.x + atomicAdd(a.sched, 1);
+    };
+    auto finish = [&]() {
+      if (a.sched == nullptr) return;
+      __threadfence();
+      if (atomicAdd(a.sched + 1, 1) == (int)gridDim.x - 1) {  // the last CTA zeroes the counters
+        __threadfence();
+        atomicExch(a.sched, 0);
+        atomicExch(a.sched + 1, 0);
+      }
+    };
+    if (lead) {
+      nexttile = tile;
+      nexttile = claim();
+    }
     CMTile t = tile_geo(tile);
     // 16-byte staging needs 16-byte aligned field bases (even-length records
     // keep every node and chunk offset even from there)
     const bool base_al16 = ((reinterpret_cast<uintptr_t>(a.f0.base) | reinterpret_cast<uintptr_t>(a.f1.base)) & 15) == 0;
-    for (int g = 0; g < nstages; ++g) {
+    for (int g = 0;; ++g) {
       const int b = g % NS;
       if (g >= NS) {  // wait for the slot, draining finished output slabs meanwhile
         while (true) {
@@ -512,6 +565,12 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
         }
       } else {
         try_drain();
+      }
+      if (tile >= ntiles) {  // end of the sequence: wake the consumers on it (they read s_tile and exit)
+        mbar_arrive(&full[b]);
+        mbar_arrive(&full[b]);
+        ktot = kp;
+        break;
       }
       double* cb = smem + b * C::SBUF;
       const int slot = ch * KC + e;  // input slot: field 0 in [0, K0), field 1 in [K0, 4 NK)
@@ -620,7 +679,16 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       mbar_arrive_cp_async(&full[b]);  // fires when this lane's copies have landed
       if (++ch == NCH) {
         ch = 0;
-        tile += gridDim.x;
+        ++kp;
+        if (lead) {
+          s_tile[kp % C::QT] = nexttile;
+          if (nexttile < ntiles)
+            nexttile = claim();
+          else
+            finish();
+        }
+        asm volatile("bar.sync 1, %0;\n" ::"n"(NPL) : "memory");  // producers: s_tile[kp] published
+        tile = s_tile[kp % C::QT];
         if (tile < ntiles) t = tile_geo(tile);
       }
     }
@@ -628,10 +696,11 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
     while (!C::OWN) {
       bool left = false;
 #pragma unroll
-      for (int j = 0; j < NW / C::NPW; ++j) left |= dtile[j] < ntiles;
+      for (int j = 0; j < NW / C::NPW; ++j) left |= dk[j] < ktot;
       if (!left) break;
       if (!try_drain()) __nanosleep(HW_CM_SLEEP);
     }
+    HW_CM_STAMP_END();
     return;
   }
 
@@ -652,11 +721,17 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
 #pragma unroll
     for (int n = 0; n < NT; ++n) acc[t][n][0] = acc[t][n][1] = 0.0;
 
-  int tile = blockIdx.x, ch = 0, k = 0;  // k = this warp's tile count
-  CMTile cg = tile_geo(tile);
+  int ch = 0, k = 0;  // k = this warp's tile count
+  CMTile cg;
   double* slab = slabs + warp * C::SLAB;
-  for (int g = 0; g < nstages; ++g) {
+  for (int g = 0;; ++g) {
     const int b = g % NS;
+    if (ch == 0) {  // a new tile: its id is published with its first chunk
+      mbar_wait(&full[b], (g / NS) & 1);
+      const int tile = s_tile[k % C::QT];
+      if (tile >= ntiles) break;
+      cg = tile_geo(tile);
+    }
     if (ch == NCH - 1) {
       // The tile's last chunk: the previous tile's slab must be drained before
       // this tile's epilogue reuses it (and, for kCons, before its `previous`
@@ -674,7 +749,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
         }
       }
     }
-    mbar_wait(&full[b], (g / NS) & 1);
+    if (ch != 0) mbar_wait(&full[b], (g / NS) & 1);
     const double* cb = smem + b * C::SBUF;
     const double* wb = C::WRES ? smem + C::WRES0 + ch * KSC * NT * 32 : cb + C::CBUF;
     // One chunk of NKS k-steps, software-pipelined: the shared-memory
@@ -820,12 +895,11 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
     if (ch == NCH - 1) {
       ++k;
       ch = 0;
-      tile += gridDim.x;
-      if (tile < ntiles) cg = tile_geo(tile);
     } else {
       ++ch;
     }
   }
+  HW_CM_STAMP_END();
 }
 
 }  // namespace hw

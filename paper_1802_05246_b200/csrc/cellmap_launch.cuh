@@ -5,10 +5,42 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <mutex>
 
 #include "cellmap.cuh"
 
 namespace hw {
+
+// Counters of the dynamic tile schedule (cellmap_kernel): kSchedSlots pairs
+// per device, zeroed once; each launch takes the next pair round robin and
+// its last CTA zeroes it again.  Launches in flight at the same time (other
+// streams, the next step under programmatic dependent launch) use different
+// pairs unless kSchedSlots launches are in flight together.
+constexpr int kSchedSlots = 256;
+inline cudaError_t sched_slot(int dev, int** out) {
+  constexpr int kDevs = 64;
+  static std::atomic<int*> base[kDevs];
+  static std::atomic<unsigned> seq[kDevs];
+  if (dev >= kDevs) {
+    *out = nullptr;  // static schedule
+    return cudaSuccess;
+  }
+  int* p = base[dev].load(std::memory_order_acquire);
+  if (p == nullptr) {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> g(mu);
+    p = base[dev].load(std::memory_order_acquire);
+    if (p == nullptr) {
+      cudaError_t e;
+      if ((e = cudaMalloc(&p, 2 * kSchedSlots * sizeof(int))) != cudaSuccess) return e;
+      if ((e = cudaMemset(p, 0, 2 * kSchedSlots * sizeof(int))) != cudaSuccess) return e;
+      if ((e = cudaDeviceSynchronize()) != cudaSuccess) return e;
+      base[dev].store(p, std::memory_order_release);
+    }
+  }
+  *out = p + 2 * (seq[dev].fetch_add(1, std::memory_order_relaxed) % kSchedSlots);
+  return cudaSuccess;
+}
 
 // Persistent grid: one wave of CTAs (SM count x resident CTAs per SM).
 template <int M, int SCH>
@@ -45,6 +77,9 @@ cudaError_t launch_cellmap(const CellMapArgs& a, cudaStream_t st) {
   int64_t nblk = cached - 1;
   if (nblk > ntiles) nblk = ntiles;
   if (nblk <= 0) return cudaSuccess;
+  CellMapArgs args = a;
+  args.sched = nullptr;  // static round-robin tile schedule
+  if (cm_dyn(SCH, M) && (e = sched_slot(dev, &args.sched)) != cudaSuccess) return e;
 #if HW_CM_PDL
   // Programmatic stream serialisation: this grid may be scheduled before the
   // previous kernel in the stream has finished; the kernel's
@@ -59,9 +94,9 @@ cudaError_t launch_cellmap(const CellMapArgs& a, cudaStream_t st) {
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
-  return cudaLaunchKernelEx(&lc, kern, a);
+  return cudaLaunchKernelEx(&lc, kern, args);
 #else
-  kern<<<(unsigned)nblk, C::NTHREADS, C::SMEM, st>>>(a);
+  kern<<<(unsigned)nblk, C::NTHREADS, C::SMEM, st>>>(args);
   return cudaGetLastError();
 #endif
 }

@@ -118,4 +118,18 @@ constexpr bool cm_self(int sch, int m) {
   return sch != 2 && m == 3;
 }
 
+// Dynamic tile schedule (a global tile counter, cellmap_kernel) instead of
+// static round robin.  The persistent CTAs of a static schedule finish up to
+// 11% apart (tools/cta_times.cu, m = 4, 1024^2); claiming tiles evens that
+// out: +4% at diss m = 4 (1024^2), +3% at m = 3, 5, +0.4-0.8% at m = 6..8,
+// +5% cons m = 3, +0.5% cons m = 8.  Static stays where the claimed order
+// measured slower per tile: diss m = 2 (HBM-bound, -7%) and cons m = 5 (-2%)
+// (profiles/ab_r01_kernel_knobs.txt).
+constexpr bool cm_dyn(int sch, int m) {
+#ifdef HW_CM_DYN
+  if (cm_knob(sch, m)) return HW_CM_DYN;
+#endif
+  return !(sch == 0 && m <= 2) && !(sch == 1 && m == 5);
+}
+
 }  // namespace hw
