@@ -12,7 +12,7 @@ HDRS := $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.h) include/hermb200.h
 KERN := $(patsubst $(SRC)/%.cu,$(BUILD)/%.o,$(wildcard $(SRC)/kern_m*.cu))
 OBJ := $(BUILD)/capi.o $(BUILD)/tables.o $(BUILD)/cellmap.o $(KERN)
 
-all: $(LIB) tools/fp64_peak
+all: $(LIB)
 
 $(BUILD)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(BUILD)
@@ -30,7 +30,8 @@ clean:
 
 .PHONY: all clean tools
 
+# probe tools link the shared cudart (no static runtime copied into the tree)
 tools/fp64_peak: tools/fp64_peak.cu
-	$(NVCC) $(ARCH) -O3 -o $@ $<
+	$(NVCC) $(ARCH) -O3 -cudart shared -o $@ $<
 
 tools: tools/fp64_peak

@@ -153,6 +153,9 @@ static DevMap device_map(int scheme, int m, double dt, double hx, double hy, dou
     cuda_check(cudaMemcpy(d.wfrag, wf.data(), wf.size() * sizeof(double), cudaMemcpyHostToDevice), "upload wfrag");
     cuda_check(cudaMemcpy(d.ocode, oc.data(), oc.size() * sizeof(int), cudaMemcpyHostToDevice), "upload ocode");
     cuda_check(cudaMemcpy(d.icode, ic.data(), ic.size() * sizeof(int), cudaMemcpyHostToDevice), "upload icode");
+    // a pageable H2D cudaMemcpy may return before its DMA lands, and the kernel
+    // runs on the caller's (possibly non-blocking) stream: wait once per new map
+    cuda_check(cudaDeviceSynchronize(), "upload map");
   } catch (...) {
     free_map(d);
     throw;
@@ -360,6 +363,7 @@ static const double* device_hl(int mu) {
   double* d = nullptr;
   cuda_check(cudaMalloc(&d, h.size() * sizeof(double)), "cudaMalloc(hl)");
   cuda_check(cudaMemcpy(d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice), "cudaMemcpy(hl)");
+  cuda_check(cudaDeviceSynchronize(), "upload hl");  // see device_map
   hl_cache()[key] = d;
   return d;
 }
@@ -506,10 +510,10 @@ static double cell_quadrature_2d(const hw_rows2d* src, int mx, int my, const hw_
   cuda_check(cudaMalloc(&dgx.p, npts * 8), "cudaMalloc");
   cuda_check(cudaMalloc(&dgw.p, npts * 8), "cudaMalloc");
   cuda_check(cudaMalloc(&dpart.p, nblk * 8), "cudaMalloc");
-  cuda_check(cudaMemcpy(dex.p, ex.data(), ex.size() * 8, cudaMemcpyHostToDevice), "cudaMemcpy");
-  cuda_check(cudaMemcpy(dey.p, ey.data(), ey.size() * 8, cudaMemcpyHostToDevice), "cudaMemcpy");
-  cuda_check(cudaMemcpy(dgx.p, gx.data(), npts * 8, cudaMemcpyHostToDevice), "cudaMemcpy");
-  cuda_check(cudaMemcpy(dgw.p, gw.data(), npts * 8, cudaMemcpyHostToDevice), "cudaMemcpy");
+  cuda_check(cudaMemcpyAsync(dex.p, ex.data(), ex.size() * 8, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
+  cuda_check(cudaMemcpyAsync(dey.p, ey.data(), ey.size() * 8, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
+  cuda_check(cudaMemcpyAsync(dgx.p, gx.data(), npts * 8, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
+  cuda_check(cudaMemcpyAsync(dgw.p, gw.data(), npts * 8, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
   L2Err2DArgs a;
   std::memset(&a, 0, sizeof(a));
   a.f = to_rows(src);
@@ -641,11 +645,13 @@ static Energy1DArgs energy_args(int mu, int64_t n_src, int parity, const hw_axis
 }
 
 // Gauss rule (host arrays) -> device copies owned by the caller's DevBufs.
-static void upload_rule(Energy1DArgs& a, const double* gx, const double* gw, DevBuf& dx, DevBuf& dw) {
+static void upload_rule(Energy1DArgs& a, const double* gx, const double* gw, DevBuf& dx, DevBuf& dw,
+                        cudaStream_t st) {
   cuda_check(cudaMalloc(&dx.p, a.npts * 8), "cudaMalloc");
   cuda_check(cudaMalloc(&dw.p, a.npts * 8), "cudaMalloc");
-  cuda_check(cudaMemcpy(dx.p, gx, a.npts * 8, cudaMemcpyHostToDevice), "cudaMemcpy");
-  cuda_check(cudaMemcpy(dw.p, gw, a.npts * 8, cudaMemcpyHostToDevice), "cudaMemcpy");
+  // stream-ordered before the kernel that reads them (pageable sources are staged before return)
+  cuda_check(cudaMemcpyAsync(dx.p, gx, a.npts * 8, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
+  cuda_check(cudaMemcpyAsync(dw.p, gw, a.npts * 8, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
   a.gx = dx.p;
   a.gw = dw.p;
 }
@@ -659,9 +665,9 @@ int hw_seminorm1d(const double* f, int mu, int64_t n_src, int parity, const hw_a
     a.f = f;
     a.order = order;
     a.scale = scale;
-    DevBuf dx, dw;
-    upload_rule(a, gx, gw, dx, dw);
     cudaStream_t st = (cudaStream_t)stream;
+    DevBuf dx, dw;
+    upload_rule(a, gx, gw, dx, dw, st);
     const int64_t nblk = (a.nt + kRedThreads - 1) / kRedThreads;
     DevBuf part;
     cuda_check(cudaMalloc(&part.p, nblk * 8), "cudaMalloc");
@@ -684,9 +690,9 @@ int hw_cons_energy1d(const double* cur, const double* prev, int m, int64_t n_src
     a.offg = src_offset(parity_cur == HW_PRIMAL ? HW_DUAL : HW_PRIMAL);
     a.order = m + 1;
     a.delta = delta;
-    DevBuf dx, dw;
-    upload_rule(a, gx, gw, dx, dw);
     cudaStream_t st = (cudaStream_t)stream;
+    DevBuf dx, dw;
+    upload_rule(a, gx, gw, dx, dw, st);
     const int64_t nblk = (a.nt + kRedThreads - 1) / kRedThreads;
     DevBuf part;
     cuda_check(cudaMalloc(&part.p, nblk * 8), "cudaMalloc");

@@ -3,6 +3,8 @@ streams; every numerical operation runs in libhermb200.so)."""
 
 from __future__ import annotations
 
+import warnings
+
 import numpy as np
 
 from ._lib import HermiteLibError
@@ -54,7 +56,15 @@ class Staging:
             if a.device != self.device:
                 raise ValueError("all fields of one call must live on the same device")
             return a.contiguous() if not a.is_contiguous() else a
-        host = t.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        if a.flags.writeable:
+            host = t.from_numpy(a)
+        else:
+            # frozen Field values are read-only views; the tensor is only ever
+            # a copy source, so wrapping it without a write flag is safe
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore", UserWarning)
+                host = t.from_numpy(a)
         # pinned host memory (e.g. torch pin_memory buffers viewed as numpy)
         # copies asynchronously on the current stream; pageable memory is
         # staged by the driver and returns once copied

@@ -5,8 +5,8 @@ Drop-in replacements for
   hermwave.conservative.full_step_conservative        (conservative.py:139-157)
   hermwave.conservative.bootstrap_first_half          (conservative.py:166-195)
 with the same signatures, validation, parity flip and time bookkeeping.  The
-arithmetic runs in one fused sm_100a kernel per call (csrc/diss2d.cuh,
-csrc/taps2d.cuh, csrc/line1d.cuh) behind the C ABI of include/hermb200.h.
+arithmetic runs in one fused sm_100a kernel per call (2D: the cell-map kernel
+of csrc/cellmap.cuh; 1D: csrc/line1d.cuh) behind the C ABI of include/hermb200.h.
 
 ``advance_*`` run many half steps on device-resident state with two
 ping-pong buffers (the throughput path used by bench.py).
