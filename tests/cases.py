@@ -46,6 +46,25 @@ X1D = (-0.4, 1.1)
 
 PERIODIC_BC = ("periodic", "periodic", 0.0, 0.0)
 
+# BASELINE config C3's setup (tests/golden/make_golden_c3.py -> c3walls.npz): conservative
+# scheme, Dirichlet x / Neumann y walls on the unit square, odd orders from both parities.
+# (name, m, n, parity of the current level, steps, kind)
+C3_CASES = [
+    ("wave_m5_primal", 5, 24, PRIMAL, 8, "wave"),
+    ("wave_m5_dual", 5, 24, DUAL, 8, "wave"),
+    ("wave_m3_primal", 3, 20, PRIMAL, 8, "wave"),
+    ("wave_m3_dual", 3, 16, DUAL, 8, "wave"),
+    ("wave_m7_primal", 7, 12, PRIMAL, 8, "wave"),
+    ("wave_m7_dual", 7, 12, DUAL, 8, "wave"),
+    ("rand_m5_primal", 5, 10, PRIMAL, 8, "rand"),
+    ("rand_m5_dual", 5, 10, DUAL, 8, "rand"),
+    ("rand_m7_primal", 7, 8, PRIMAL, 6, "rand"),
+    ("rand_m7_dual", 7, 8, DUAL, 6, "rand"),
+]
+C3_LAM = 0.9
+C3_WAVE_BC = (("dirichlet0", "dirichlet0", 0.0, 0.0), ("neumann0", "neumann0", 0.0, 0.0))
+C3_RAND_BC = (("dirichlet0", "dirichlet0", 0.3, -0.2), ("neumann0", "neumann0", 0.0, 0.0))
+
 
 def forcing_fn(l, s, x, t):
     import numpy as np

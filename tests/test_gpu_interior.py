@@ -32,8 +32,7 @@ def setup(m, walls, par, seed):
     return grid, bc, obx, oby, rng, shp
 
 
-CASES = [(m, walls, par) for m in range(1, 9) for walls, par in ((False, O.PRIMAL), (True, O.DUAL), (True, O.PRIMAL))
-         if not (walls and par == O.PRIMAL and m % 2)]
+CASES = [(m, walls, par) for m in range(1, 9) for walls, par in ((False, O.PRIMAL), (True, O.DUAL), (True, O.PRIMAL))]
 
 
 @pytest.mark.parametrize("m,walls,par", CASES)
