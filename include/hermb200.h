@@ -73,7 +73,7 @@ typedef struct {
 
 /* Library info. */
 const char* hw_last_error(void);
-int hw_version(void);              /* 3: + 2D seminorm, lower-level batched API */
+int hw_version(void);              /* 4: + hw_inner2d (2D conservative energy) */
 int hw_max_order(void);            /* largest m with a compiled fast path */
 
 /* interp.py:51-75 interp_matrix(mu): (2mu+2)^2 row-major, exact doubles. */
@@ -175,6 +175,25 @@ int hw_seminorm2d(const hw_rows2d* src, int mx, int my, const hw_geom2d* geom,
                   double hx, double hy, int dx, int dy, int npts,
                   const double* gauss_x, const double* gauss_w,
                   double* out_host, void* stream);
+
+/*
+ * Bilinear 2D seminorm: sum over the target cells [trow0, trow0+ntrows) of
+ * the field's corner gather of w_cell * int int (D I f)(D I g) dx dy, with
+ * D = d^dx/dx^dx d^dy/dy^dy and I = I_{mx,my} the tensor interpolant, by
+ * npts^2-point Gauss quadrature (exact for 2 npts - 1 >= 2 (2 m + 1) - dx - dy
+ * per axis).  g = NULL means g = f.  wall_half != 0: a cell whose gather used
+ * a wall ghost (dual parity on a wall grid) straddles the wall and counts
+ * 1/2 per such axis, i.e. the integral over the physical domain of the
+ * reflected extension the ghosts define (boundary.py:56-98).  Accumulated in
+ * double-double.  The building block of the 2D conservative energy
+ * (norms.py conservative_energy_2d; the reference's conservative_energy,
+ * diagnostics.py:190-226, is 1D and periodic only).  Slabs: pass a row window
+ * with halos and sum the per-rank results.  -> *out_host after a stream sync.
+ */
+int hw_inner2d(const hw_rows2d* f, const hw_rows2d* g, int mx, int my, const hw_geom2d* geom,
+               double hx, double hy, int dx, int dy, int npts,
+               const double* gauss_x, const double* gauss_w, int wall_half,
+               double* out_host, void* stream);
 
 /*
  * diagnostics.py:66-115 per-piece 1D L2 errors.  For each target piece t the

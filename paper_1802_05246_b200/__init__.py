@@ -28,6 +28,7 @@ from .norms import (
     PlaneWave2D,
     StandingWave2D,
     conservative_energy,
+    conservative_energy_2d,
     default_npts,
     dissipative_energy,
     dissipative_energy_2d,
@@ -58,7 +59,7 @@ __all__ = [
     "PascalTable", "apply_interp", "apply_interp_2d", "conservative_update_1d", "conservative_update_2d",
     "eval_series", "expand_taylor", "expand_taylor_2d", "ghost_data", "ghost_data_2d", "pascal_table",
     "ErrorReport", "PlaneWave2D", "StandingWave2D", "default_npts", "fit_rate", "gauss_rule",
-    "dissipative_energy", "dissipative_energy_2d", "conservative_energy",
+    "dissipative_energy", "dissipative_energy_2d", "conservative_energy", "conservative_energy_2d",
     "l2_error_field", "l2_error_field_2d", "l2_errors_pair",
     "NumericalError", "advance_2d", "advance_conservative", "bootstrap_first_half",
     "full_step_conservative", "half_step_1d", "half_step_2d", "interp_matrix", "require_finite",

@@ -253,7 +253,7 @@ using namespace hw;
 extern "C" {
 
 const char* hw_last_error(void) { return g_err.c_str(); }
-int hw_version(void) { return 3; }
+int hw_version(void) { return 4; }
 int hw_max_order(void) { return kMaxFast; }
 
 int hw_interp_matrix(int mu, double* out) {
@@ -469,6 +469,29 @@ static double reduce_partials(double* part, int64_t n, cudaStream_t st) {
   return h;
 }
 
+// Ex[p][c] = sum_a d^d/dxi^d (xi_p)^a M[a][c] / h^d at xi_p = xg_p / 2
+// (diagnostics.py:128-130 at d = 0): the tensor interpolant's d-th derivative
+// at the Gauss points, as a map of the cell's stacked corner data.
+static std::vector<double> deriv_eval_matrix(int mu, int d, double h, const std::vector<double>& gx) {
+  const std::vector<double> M = hermite_matrix(mu);
+  const int n = 2 * mu + 2, npts = (int)gx.size();
+  std::vector<double> e((size_t)npts * n, 0.0);
+  for (int p = 0; p < npts; ++p) {
+    const double xi = 0.5 * gx[p];
+    for (int c = 0; c < n; ++c) {
+      double s = 0.0, pw = 1.0;
+      for (int a2 = d; a2 < n; ++a2) {
+        double fall = 1.0;  // a2! / (a2 - d)!
+        for (int k = 0; k < d; ++k) fall *= (double)(a2 - k);
+        s += fall * pw * M[(size_t)a2 * n + c];
+        pw *= xi;
+      }
+      e[(size_t)p * n + c] = d ? s * std::pow(h, -(double)d) : s;
+    }
+  }
+  return e;
+}
+
 // Shared by hw_l2err2d and hw_seminorm2d: the tensor interpolant of every
 // target cell evaluated at the npts^2 Gauss points, d-th derivative along each
 // axis (d = 0: the values), reduced to sum_cells sum_pq w_p w_q (val - exact)^2.
@@ -482,26 +505,7 @@ static double cell_quadrature_2d(const hw_rows2d* src, int mx, int my, const hw_
   std::vector<double> gx(npts), gw(npts);
   cuda_check(cudaMemcpy(gx.data(), gauss_x, npts * sizeof(double), cudaMemcpyDefault), "copy gauss x");
   cuda_check(cudaMemcpy(gw.data(), gauss_w, npts * sizeof(double), cudaMemcpyDefault), "copy gauss w");
-  auto emat = [&](int mu, int d, double h) {
-    const std::vector<double> M = hermite_matrix(mu);
-    const int n = 2 * mu + 2;
-    std::vector<double> e((size_t)npts * n, 0.0);
-    for (int p = 0; p < npts; ++p) {
-      const double xi = 0.5 * gx[p];
-      for (int c = 0; c < n; ++c) {
-        double s = 0.0, pw = 1.0;
-        for (int a2 = d; a2 < n; ++a2) {
-          double fall = 1.0;  // a2! / (a2 - d)!
-          for (int k = 0; k < d; ++k) fall *= (double)(a2 - k);
-          s += fall * pw * M[(size_t)a2 * n + c];
-          pw *= xi;
-        }
-        e[(size_t)p * n + c] = d ? s * std::pow(h, -(double)d) : s;
-      }
-    }
-    return e;
-  };
-  const std::vector<double> ex = emat(mx, dx, hx), ey = emat(my, dy, hy);
+  const std::vector<double> ex = deriv_eval_matrix(mx, dx, hx, gx), ey = deriv_eval_matrix(my, dy, hy, gx);
   const int64_t ncell = g.ntx * g.nty;
   const int64_t nblk = (ncell + kRedThreads - 1) / kRedThreads;
   DevBuf dex, dey, dgx, dgw, dpart;
@@ -577,6 +581,73 @@ int hw_seminorm2d(const hw_rows2d* src, int mx, int my, const hw_geom2d* geom, d
     const double s = cell_quadrature_2d(src, mx, my, geom, 0.0, 0.0, hx, hy, dx, dy, npts, gauss_x, gauss_w, 3,
                                         nullptr, nullptr, (cudaStream_t)stream);
     *out_host = s * (0.25 * hx * hy);
+  });
+}
+
+int hw_inner2d(const hw_rows2d* f, const hw_rows2d* g, int mx, int my, const hw_geom2d* geom, double hx, double hy,
+               int dx, int dy, int npts, const double* gauss_x, const double* gauss_w, int wall_half,
+               double* out_host, void* stream) {
+  return guard([&] {
+    HW_CHECK(f && f->base && gauss_x && gauss_w && out_host, "null pointer");
+    HW_CHECK(!g || g->base, "null field pointer");
+    HW_CHECK(mx >= 0 && my >= 0 && mx <= kMaxOrder && my <= kMaxOrder, "orders out of range");
+    HW_CHECK(dx >= 0 && dy >= 0 && dx <= 2 * mx + 1 && dy <= 2 * my + 1, "derivative orders out of range");
+    HW_CHECK(npts >= 1 && npts <= 64, "npts out of range");
+    const Geo gg = check_geom(geom);
+    check_rows(f, gg);
+    if (g) check_rows(g, gg, f);
+    cudaStream_t st = (cudaStream_t)stream;
+    *out_host = 0.0;
+    const int64_t ncell = gg.ntrows * gg.nty;
+    if (ncell == 0) return;
+    std::vector<double> gx(gauss_x, gauss_x + npts), gw(gauss_w, gauss_w + npts);
+    const std::vector<double> ex = deriv_eval_matrix(mx, dx, hx, gx), ey = deriv_eval_matrix(my, dy, hy, gx);
+    const int64_t nblk = (ncell + kRedThreads - 1) / kRedThreads;
+    DevBuf dex, dey, dgw, dpart, dout;
+    cuda_check(cudaMalloc(&dex.p, ex.size() * 8), "cudaMalloc");
+    cuda_check(cudaMalloc(&dey.p, ey.size() * 8), "cudaMalloc");
+    cuda_check(cudaMalloc(&dgw.p, npts * 8), "cudaMalloc");
+    cuda_check(cudaMalloc(&dpart.p, nblk * 16), "cudaMalloc");
+    cuda_check(cudaMalloc(&dout.p, 8), "cudaMalloc");
+    cuda_check(cudaMemcpyAsync(dex.p, ex.data(), ex.size() * 8, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
+    cuda_check(cudaMemcpyAsync(dey.p, ey.data(), ey.size() * 8, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
+    cuda_check(cudaMemcpyAsync(dgw.p, gw.data(), npts * 8, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
+    Inner2DArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.f = to_rows(f);
+    a.g = g ? to_rows(g) : a.f;
+    a.same = g == nullptr || (g->base == f->base && g->halo_lo == f->halo_lo && g->halo_hi == f->halo_hi);
+    a.nx = gg.nx;
+    a.ny = gg.ny;
+    a.nty = gg.nty;
+    a.trow0 = gg.trow0;
+    a.ntrows = gg.ntrows;
+    a.off = gg.off;
+    a.periodic = gg.periodic;
+    a.kxl = gg.periodic ? 0 : geom->bcx.left_kind;
+    a.kxh = gg.periodic ? 0 : geom->bcx.right_kind;
+    a.kyl = gg.periodic ? 0 : geom->bcy.left_kind;
+    a.kyh = gg.periodic ? 0 : geom->bcy.right_kind;
+    a.gxl = geom->bcx.left_value;
+    a.gxh = geom->bcx.right_value;
+    a.gyl = geom->bcy.left_value;
+    a.gyh = geom->bcy.right_value;
+    a.mx = mx;
+    a.my = my;
+    a.npts = npts;
+    a.wall_half = wall_half != 0;
+    a.ex = dex.p;
+    a.ey = dey.p;
+    a.gw = dgw.p;
+    a.part = dpart.p;
+    inner2d_kernel<<<(unsigned)nblk, kRedThreads, 0, st>>>(a);
+    cuda_check(cudaGetLastError(), "inner2d launch");
+    sum_partials_dd_kernel<<<1, kRedThreads, 0, st>>>(dpart.p, nblk, dout.p);
+    cuda_check(cudaGetLastError(), "sum_partials_dd launch");
+    double h = 0.0;
+    cuda_check(cudaMemcpyAsync(&h, dout.p, sizeof(double), cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+    cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    *out_host = h;
   });
 }
 

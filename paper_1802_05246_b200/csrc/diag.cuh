@@ -109,6 +109,139 @@ __global__ void l2err2d_kernel(L2Err2DArgs a) {
   if (threadIdx.x == 0) a.part[blockIdx.x] = bs;
 }
 
+// ---------------------------------------------------------------- bilinear seminorm (conservative energy)
+// Compensated (double-double) accumulation: the 2D conservative energy is a
+// difference of O(1) inner products that cancel to O((omega dt)^2), so the
+// reduction itself must not add O(log N eps) relative error.
+__device__ inline void two_sum(double a, double b, double& s, double& e) {
+  s = a + b;
+  const double bb = s - a;
+  e = (a - (s - bb)) + (b - bb);
+}
+
+__device__ inline void dd_add(double& hi, double& lo, double x) {
+  double s, e;
+  two_sum(hi, x, s, e);
+  hi = s;
+  lo += e;
+}
+
+// Deterministic double-double block reduction (fixed tree order); sh holds 2 * blockDim doubles.
+__device__ inline void block_sum_dd(double& hi, double& lo, double* sh) {
+  sh[threadIdx.x] = hi;
+  sh[blockDim.x + threadIdx.x] = lo;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) {
+      double h, e;
+      two_sum(sh[threadIdx.x], sh[threadIdx.x + s], h, e);
+      e += sh[blockDim.x + threadIdx.x] + sh[blockDim.x + threadIdx.x + s];
+      double h2, e2;
+      two_sum(h, e, h2, e2);
+      sh[threadIdx.x] = h2;
+      sh[blockDim.x + threadIdx.x] = e2;
+    }
+    __syncthreads();
+  }
+  hi = sh[0];
+  lo = sh[blockDim.x];
+  __syncthreads();
+}
+
+__global__ void sum_partials_dd_kernel(const double* part, int64_t n, double* out) {
+  __shared__ double sh[2 * kRedThreads];
+  double hi = 0.0, lo = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    dd_add(hi, lo, part[2 * i]);
+    lo += part[2 * i + 1];
+  }
+  block_sum_dd(hi, lo, sh);
+  if (threadIdx.x == 0) *out = hi + lo;
+}
+
+struct Inner2DArgs {
+  Rows f, g;
+  int same;  // g aliases f
+  int64_t nx, ny, nty, trow0, ntrows;
+  int off, periodic;
+  int kxl, kxh, kyl, kyh;
+  double gxl, gxh, gyl, gyh;
+  int mx, my, npts, wall_half;
+  const double* ex;  // as L2Err2DArgs (derivative evaluation matrices, 1/h^d folded in)
+  const double* ey;
+  const double* gw;
+  double* part;      // (hi, lo) per block
+};
+
+// T[sx*wx + k] = sum_{sy,l} Ey[q][sy,l] U[sx][sy][k][l] for one field of one cell.
+__device__ inline void cell_ycontract(const RowRef* const* rr, const ColRef* const* cc, int wx, int wy, int P,
+                                      const double* ey, int q, double* T) {
+  for (int sx = 0; sx < 2; ++sx)
+    for (int k = 0; k < wx; ++k) {
+      double s = 0.0;
+      for (int sy = 0; sy < 2; ++sy)
+        for (int l = 0; l < wy; ++l) {
+          double val = rr[sx]->p[cc[sy]->c * P + k * wy + l];
+          if (rr[sx]->kind | cc[sy]->kind)
+            val = ghosted(val, k, l, rr[sx]->kind, rr[sx]->g, cc[sy]->kind, cc[sy]->g);
+          s = fma(__ldg(ey + q * 2 * wy + sy * wy + l), val, s);
+        }
+      T[sx * wx + k] = s;
+    }
+}
+
+// sum_cells w_cell int int (D I f)(D I g), D = d_x^dx d_y^dy folded into Ex/Ey,
+// over target rows [trow0, trow0 + ntrows) of the field's corner gather.
+// wall_half: cells whose gather used a wall ghost (dual parity) straddle the
+// wall and count 1/2 per such axis (the integral over the physical domain of
+// the reflected extension the ghosts define, boundary.py:56-98).
+__global__ void inner2d_kernel(Inner2DArgs a) {
+  __shared__ double sh[2 * kRedThreads];
+  const int64_t ncell = a.ntrows * a.nty;
+  const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double hi = 0.0, lo = 0.0;
+  if (cell < ncell) {
+    const int64_t ti = a.trow0 + cell / a.nty, tj = cell % a.nty;
+    const int mx = a.mx, my = a.my, wx = mx + 1, wy = my + 1, P = wx * wy;
+    const int64_t sx0 = ti + a.off, sy0 = tj + a.off;
+    RowRef fr[2], gr[2];
+    ColRef cl[2];
+    for (int s = 0; s < 2; ++s) {
+      fr[s] = resolve_row(a.f, sx0 + s, a.nx, a.ny * P, a.periodic, a.kxl, a.kxh, a.gxl, a.gxh);
+      gr[s] = resolve_row(a.g, sx0 + s, a.nx, a.ny * P, a.periodic, a.kxl, a.kxh, a.gxl, a.gxh);
+      cl[s] = resolve_col(sy0 + s, a.ny, a.periodic, a.kyl, a.kyh, a.gyl, a.gyh);
+    }
+    const RowRef* frp[2] = {&fr[0], &fr[1]};
+    const RowRef* grp[2] = {&gr[0], &gr[1]};
+    const ColRef* clp[2] = {&cl[0], &cl[1]};
+    double wcell = 1.0;
+    if (a.wall_half && !a.periodic) {
+      if (sx0 < 0 || sx0 + 1 > a.nx - 1) wcell *= 0.5;
+      if (sy0 < 0 || sy0 + 1 > a.ny - 1) wcell *= 0.5;
+    }
+    double Tf[2 * 13], Tg[2 * 13];
+    for (int q = 0; q < a.npts; ++q) {
+      cell_ycontract(frp, clp, wx, wy, P, a.ey, q, Tf);
+      if (!a.same) cell_ycontract(grp, clp, wx, wy, P, a.ey, q, Tg);
+      const double* tg = a.same ? Tf : Tg;
+      for (int p = 0; p < a.npts; ++p) {
+        double vf = 0.0, vg = 0.0;
+        for (int e = 0; e < 2 * wx; ++e) {
+          const double x = __ldg(a.ex + p * 2 * wx + e);
+          vf = fma(x, Tf[e], vf);
+          vg = fma(x, tg[e], vg);
+        }
+        dd_add(hi, lo, wcell * a.gw[p] * a.gw[q] * vf * vg);
+      }
+    }
+  }
+  block_sum_dd(hi, lo, sh);
+  if (threadIdx.x == 0) {
+    a.part[2 * blockIdx.x] = hi;
+    a.part[2 * blockIdx.x + 1] = lo;
+  }
+}
+
 struct L2Err1DArgs {
   const double* f;
   int64_t n, nt;

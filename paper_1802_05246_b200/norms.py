@@ -275,6 +275,86 @@ def conservative_energy(current: Field1D, previous: Field1D, speed: float, dt: f
     return out.value
 
 
+def _inner2d(f, g, grid, parity: str, bc: BoundarySpec2D, orders, dx: int, dy: int, npts: int, st,
+             trow0: int = 0, ntrows: int = -1, rows_f=None, rows_g=None) -> float:
+    """hw_inner2d: sum_cells w_cell int int (D I f)(D I g) over the field's cells
+    (wall cells counted over their physical half; slabs pass row windows)."""
+    xg, wg = gauss_rule(npts)
+    gx = np.ascontiguousarray(xg, dtype=np.float64)
+    gw = np.ascontiguousarray(wg, dtype=np.float64)
+    geo = geom2d(grid, parity, bc, trow0, ntrows)
+    rf = rows_f if rows_f is not None else rows2d(f)
+    rg = None if g is None else (rows_g if rows_g is not None else rows2d(g))
+    out = C.c_double(0.0)
+    L.check(L.lib().hw_inner2d(C.byref(rf), C.byref(rg) if rg is not None else None, int(orders[0]), int(orders[1]),
+                               C.byref(geo), grid.hx, grid.hy, int(dx), int(dy), int(npts),
+                               gx.ctypes.data_as(C.c_void_p), gw.ctypes.data_as(C.c_void_p), 1, C.byref(out),
+                               st.stream), "conservative_energy_2d")
+    return out.value
+
+
+def conservative_energy_2d(current: Field2D, previous: Field2D, speed: float, dt: float,
+                           bc: BoundarySpec2D) -> float:
+    """A defined 2D energy of a conservative two-level state (SURVEY §8f row 2;
+    the reference's conservative_energy, diagnostics.py:190-226, is 1D and
+    periodic only, and the paper proves conservation in 1D only).
+
+    The reference's E = |P+|^2 + |P-|^2 (P± = I a - S± I b, a = current,
+    b = previous) equals 2 (|I a|^2 + |I b|^2 - <I a, I (2 T b)>), where
+    2 T b is the scheme's own update of b with a zero previous level
+    (conservative.py:115-136): Hermite interpolation is an orthogonal
+    projection in the (m+1) seminorm, so the shifted pieces can be replaced by
+    the update (oracle.cons_energy_1d_adjoint reproduces the reference's values
+    to 1e-14, tests/test_energy.py).  In 2D the same form is taken in the mixed
+    seminorm |d_x^{m+1} d_y^{m+1} .|, in which the tensor interpolant is an
+    orthogonal projection and the wave cosine C(c dt/2) (what the update tensor
+    applies within a cell, c dt/2 <= h/2) is self-adjoint, so
+    full_step_conservative conserves
+
+        E2 = 2 (|I a|^2 + |I b|^2 - <I a, I (2 T b)>)
+
+    exactly in exact arithmetic.  Wall grids (Dirichlet / Neumann, C3): the
+    ghosts are the odd / even reflections (boundary.py:56-98), so the integral
+    runs over the physical domain, wall-straddling (ghost-padded) cells
+    counting their inner half; conservation then holds for BC-compatible data
+    (primal wall nodes carrying the reflection symmetry, which the scheme
+    itself produces and exact initial data satisfy; Dirichlet values equal on
+    walls that meet at a corner).  Inner products are exact Gauss quadrature
+    (m+1 points per axis) summed in double-double on the device."""
+    if not (isinstance(current, Field2D) and isinstance(previous, Field2D)):
+        raise ValueError("conservative_energy_2d takes 2D fields")
+    grid = current.grid
+    if previous.grid != grid:
+        raise ValueError("the two levels must live on the same grid")
+    check_periodicity(bc.x, grid.periodic)
+    check_periodicity(bc.y, grid.periodic)
+    if current.parity == previous.parity:
+        raise ValueError("the two levels must sit on opposite parities")
+    m = current.orders[0]
+    if current.orders != (m, m) or previous.orders != (m, m):
+        raise ValueError(f"levels carry orders {current.orders} and {previous.orders}, want ({m}, {m})")
+    if abs(0.5 * speed * dt) > 0.5 * min(grid.hx, grid.hy) * (1.0 + 1e-12):
+        raise ValueError("the energy needs c dt / 2 <= h / 2 (lambda <= 1)")
+    st = Staging(current.values, previous.values)
+    a = st.to_dev(current.values)
+    b = st.to_dev(previous.values)
+    tb2 = torch_zeros_like(a)
+    gb = geom2d(grid, previous.parity, bc)
+    L.check(L.lib().hw_cons2d_step(C.byref(rows2d(b)), ptr(tb2), ptr(tb2), int(m), C.byref(gb), float(dt),
+                                   grid.hx, grid.hy, float(speed), st.stream), "conservative_energy_2d")
+    npts = m + 1
+    ia = _inner2d(a, None, grid, current.parity, bc, (m, m), m + 1, m + 1, npts, st)
+    ib = _inner2d(b, None, grid, previous.parity, bc, (m, m), m + 1, m + 1, npts, st)
+    iab = _inner2d(a, tb2, grid, current.parity, bc, (m, m), m + 1, m + 1, npts, st)
+    return 2.0 * (ia + ib - iab)
+
+
+def torch_zeros_like(x):
+    import torch
+
+    return torch.zeros_like(x)
+
+
 @dataclass(frozen=True)
 class ErrorReport:
     """Refinement-study results, coarsest first (diagnostics.py:241-270)."""

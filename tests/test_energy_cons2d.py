@@ -1,0 +1,177 @@
+"""The defined 2D conservative energy (norms.conservative_energy_2d).
+
+The reference's conservative energy is 1D and periodic only (diagnostics.py:190-226).
+The 2D definition generalises its adjoint form (see oracle.cons_energy_2d), and is
+pinned by:
+  (i)   the 1D adjoint form reproduces the REFERENCE's conservative_energy on its
+        own golden states (tests/golden/energy.npz);
+  (ii)  the oracle's 2D energy is conserved to rounding by the oracle's restatement
+        of full_step_conservative (itself bitwise-pinned to the reference), on
+        periodic and on C3's wall grids, from both parities;
+  (iii) walls: the wall energy is a quarter of the periodic energy of the
+        reflected (doubled) state, the extension the ghosts define;
+  (iv)  the device reduction equals the oracle's closed-form (monomial Gram)
+        integration, and the device stepper conserves the device energy.
+"""
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+from cases import C3_RAND_BC, C3_WAVE_BC
+from oracle import hermite_oracle as O
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "energy.npz")
+X1D = (-0.4, 1.1)
+CONS = [("m1", 1, 10, O.PRIMAL, 0.9, 1.0), ("m2_dual", 2, 9, O.DUAL, 0.5, 1.3), ("m3_lam1", 3, 8, O.PRIMAL, 1.0, 1.0),
+        ("m4", 4, 11, O.DUAL, 0.7, 0.8), ("m6", 6, 6, O.PRIMAL, 0.9, 1.0)]
+BCS = {"periodic": (O.PERIODIC_BC, O.PERIODIC_BC), "c3": C3_WAVE_BC, "c3_g": C3_RAND_BC}
+
+
+@pytest.fixture(scope="module")
+def gold():
+    with np.load(GOLD) as z:
+        return {k: z[k] for k in z.files}
+
+
+@pytest.mark.parametrize("case", CONS, ids=[c[0] for c in CONS])
+def test_adjoint_form_reproduces_reference_1d_energy(gold, case):
+    name, m, n, par, lam, speed = case
+    h = (X1D[1] - X1D[0]) / n
+    dt = lam * h / speed
+    e = O.cons_energy_1d_adjoint(gold[f"ec/{name}/cur"], gold[f"ec/{name}/prev"], par, n, h, speed, dt)
+    assert e == pytest.approx(float(gold[f"ec/{name}/e"]), rel=1e-13)
+
+
+def _state(m, n, par, kind, seed):
+    """Random two-level state, BC-compatible at primal wall nodes."""
+    bx, by = BCS[kind]
+    per = kind == "periodic"
+    rng = np.random.default_rng(seed)
+    nn = lambda p: n if per or p == O.DUAL else n + 1  # noqa: E731
+    a = rng.standard_normal((nn(par), nn(par), m + 1, m + 1))
+    b = rng.standard_normal((nn(O.flip(par)), nn(O.flip(par)), m + 1, m + 1))
+    if not per:
+        if par == O.PRIMAL:
+            a = O.wall_compatible(a, bx, by)
+        else:
+            b = O.wall_compatible(b, bx, by)
+    return a, b, per, bx, by
+
+
+@pytest.mark.parametrize("kind", ["periodic", "c3", "c3_g"])
+@pytest.mark.parametrize("par", [O.PRIMAL, O.DUAL])
+@pytest.mark.parametrize("m", [1, 2, 5])
+def test_oracle_energy_2d_is_conserved(m, par, kind):
+    n, lam = 7, 0.9
+    h = 1.0 / n
+    a, b, per, bx, by = _state(m, n, par, kind, 40 + m)
+    e0 = O.cons_energy_2d(a, b, par, per, h, h, 1.0, lam * h, bx, by)
+    cur, prev, p = a, b, par
+    for _ in range(25):
+        cur, prev = O.cons_step_2d(cur, prev, p, per, h, h, m, lam, 1.0, bx, by), cur
+        p = O.flip(p)
+    e = O.cons_energy_2d(cur, prev, p, per, h, h, 1.0, lam * h, bx, by)
+    # rounding of random high-order coefficients grows with cond(M_m)
+    assert e == pytest.approx(e0, rel={5: 1e-10}.get(m, 1e-12))
+    assert e0 > 0.0
+
+
+def _double(d, par, bx, by):
+    """Reflect a wall-grid field (unit square, C3 walls) into the periodic field on
+    [-1, 1)^2 that the ghosts imply (odd in x for Dirichlet, even in y for Neumann)."""
+    sx = O.refl_signs(bx[0], d.shape[-2])
+    sy = O.refl_signs(by[0], d.shape[-1])
+
+    def axis(e, ax, s):
+        e = np.moveaxis(e, ax, 0)
+        refl = lambda blk: blk * (s[:, None] if ax == 0 else s[None, :])  # noqa: E731
+        if par == O.DUAL:     # nodes (i + 1/2) h, i = 0..n-1  ->  j = i + n, mirror j = n - 1 - i
+            out = np.concatenate([refl(e[::-1]), e])
+        else:                 # nodes i h, i = 0..n  ->  j = i + n (mod 2n), mirror j = n - i
+            n = e.shape[0] - 1
+            out = np.concatenate([e[n:n + 1], refl(e[1:n][::-1]), e[:n]])
+        return np.moveaxis(out, 0, ax)
+
+    return axis(axis(d, 0, sx), 1, sy)
+
+
+@pytest.mark.parametrize("par", [O.PRIMAL, O.DUAL])
+@pytest.mark.parametrize("m", [2, 5])
+def test_oracle_wall_energy_is_quarter_of_doubled_periodic(m, par):
+    n, lam = 6, 0.9
+    h = 1.0 / n
+    a, b, _, bx, by = _state(m, n, par, "c3", 70 + m)
+    ew = O.cons_energy_2d(a, b, par, False, h, h, 1.0, lam * h, bx, by)
+    ep = O.cons_energy_2d(_double(a, par, bx, by), _double(b, O.flip(par), bx, by), par, True, h, h, 1.0, lam * h)
+    assert 4.0 * ew == pytest.approx(ep, rel={5: 1e-11}.get(m, 1e-13))
+
+
+# ---------------------------------------------------------------- device
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["periodic", "c3", "c3_g"])
+@pytest.mark.parametrize("par", [O.PRIMAL, O.DUAL])
+@pytest.mark.parametrize("m", [1, 3, 5, 8])
+def test_device_energy_2d_matches_oracle(m, par, kind):
+    import paper_1802_05246_b200 as hb
+
+    n, lam, speed = 9, 0.8, 1.2
+    h = 1.0 / n
+    a, b, per, bx, by = _state(m, n, par, kind, 90 + m)
+    dt = lam * h / speed
+    grid = hb.Grid2D(0.0, 1.0, 0.0, 1.0, n, n, per)
+    bc = hb.BoundarySpec2D() if per else hb.BoundarySpec2D(hb.BoundarySpec(*bx), hb.BoundarySpec(*by))
+    got = hb.conservative_energy_2d(hb.Field2D(grid, par, 0.0, a), hb.Field2D(grid, hb.flip(par), -0.5 * dt, b),
+                                    speed, dt, bc)
+    want = O.cons_energy_2d(a, b, par, per, h, h, speed, dt, bx, by)
+    # Gauss vs closed-form Gram, interpolants amplified by cond(M_mu) at high m
+    assert got == pytest.approx(want, rel={8: 1e-9}.get(m, 1e-12))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("par", ["primal", "dual"])
+def test_device_c3_energy_conserved(par):
+    """C3's setup (m=5, Dirichlet x / Neumann y, standing wave) at 256^2 on the
+    device: 200 full steps keep the defined energy to 1e-10 relative (the
+    rounding floor of a difference of inner products cancelling to
+    O((omega dt)^2))."""
+    import paper_1802_05246_b200 as hb
+
+    m, n, lam = 5, 256, 0.9
+    grid = hb.Grid2D(0.0, 1.0, 0.0, 1.0, n, n, False)
+    bc = hb.BoundarySpec2D(hb.BoundarySpec(*C3_WAVE_BC[0]), hb.BoundarySpec(*C3_WAVE_BC[1]))
+    cfg = hb.SchemeConfig(m=m, lam=lam)
+    dt = cfg.dt(grid.hx)
+    pi, om = math.pi, math.pi * math.sqrt(2.0)
+    a = hb.standing_wave_on_grid(grid, par, 0.0, m, m, pi, pi, om, py=0.5 * pi)
+    b = hb.standing_wave_on_grid(grid, hb.flip(par), -0.5 * dt, m, m, pi, pi, om, py=0.5 * pi)
+    st = hb.TwoLevelState(hb.Field2D(grid, par, 0.0, a), hb.Field2D(grid, hb.flip(par), -0.5 * dt, b))
+    e0 = hb.conservative_energy_2d(st.current, st.previous, 1.0, dt, bc)
+    st = hb.advance_conservative(st, cfg, bc, 200)
+    e1 = hb.conservative_energy_2d(st.current, st.previous, 1.0, dt, bc)
+    assert abs(e1 - e0) <= 1e-10 * e0
+    # and it is the physical energy scale: E2 of the exact wave is
+    # time-independent, equal at t = 0 and after the steps to O(h^(2m)) of itself
+    a1 = hb.standing_wave_on_grid(grid, st.current.parity, st.current.time, m, m, pi, pi, om, py=0.5 * pi)
+    b1 = hb.standing_wave_on_grid(grid, st.previous.parity, st.previous.time, m, m, pi, pi, om, py=0.5 * pi)
+    ex = hb.conservative_energy_2d(hb.Field2D(grid, st.current.parity, st.current.time, a1),
+                                   hb.Field2D(grid, st.previous.parity, st.previous.time, b1), 1.0, dt, bc)
+    assert ex == pytest.approx(e0, rel=1e-6)
+
+
+@pytest.mark.gpu
+def test_device_energy_2d_cons_errors():
+    import paper_1802_05246_b200 as hb
+
+    m, n = 2, 4
+    grid = hb.Grid2D(0.0, 1.0, 0.0, 1.0, n, n, True)
+    f = hb.Field2D(grid, hb.PRIMAL, 0.0, np.zeros((n, n, m + 1, m + 1)))
+    g = hb.Field2D(grid, hb.DUAL, 0.0, np.zeros((n, n, m + 1, m + 1)))
+    with pytest.raises(ValueError, match="opposite parities"):
+        hb.conservative_energy_2d(f, f, 1.0, 0.1, hb.BoundarySpec2D())
+    with pytest.raises(ValueError, match="lambda <= 1"):
+        hb.conservative_energy_2d(f, g, 1.0, 2.0 * grid.hx, hb.BoundarySpec2D())
+    assert hb.conservative_energy_2d(f, g, 1.0, 0.1, hb.BoundarySpec2D()) == 0.0
