@@ -28,7 +28,7 @@ def test_header_symbols_exported():
 
 
 def test_version_and_orders():
-    assert L.lib().hw_version() == 3
+    assert L.lib().hw_version() == 4
     assert L.lib().hw_max_order() == 8
 
 
