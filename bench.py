@@ -158,115 +158,169 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ reference (CPU) arm
+#
+# The reference is pure Python/numpy.  It is installed UNMODIFIED into
+# baseline/_ref (pip install --no-index --target baseline/_ref
+# of /root/reference/pkg); that copy travels to the GPU box with the repo.
+# Each CPU sample runs the reference's own public hermwave.half_step_2d on a
+# periodic n x R strip with the C2 spacing (h = 1/n on both axes), m, lambda
+# and standing-wave data, i.e. R rows of the C2 grid's work: the per-node
+# arithmetic is data-independent, so DOF-updates/s of the strip is C2's rate.
+# A whole C2 half step would take the reference ~135 s and ~40 GiB (SURVEY
+# §8a row 15).  Without baseline/_ref the numpy restatement in oracle/ stands
+# in ("port").
 
-def _window(m: int, n: int, rows: int, r0: int):
-    """Source rows r0 .. r0+rows (inclusive) of the C2 standing wave."""
-    from oracle import hermite_oracle as O
-
-    h = 1.0 / n
-    x = O.nodes(0.0, h, n, True, O.PRIMAL)
-    xw = x[r0: r0 + rows + 1]
-    u = O.planewave_data(xw, x, 0.0, m, m, 1, h, h)
-    v = O.planewave_data(xw, x, 0.0, m - 1, m - 1, 1, h, h, tder=1)
-    return u, v
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+STRIP_ROWS = 4
 
 
-def _oracle_rows(u, v, m: int, n: int, lam: float = 0.9):
-    """One half step of the numpy restatement of the reference (oracle/, step
-    for step the reference's own numpy ops; pinned bitwise against the
-    reference's golden vectors) for the targets of a source-row window."""
+def _standing_blocks(xn, yn, t, k, h, tder):
+    """Scaled blocks (h^a/a!)(h^b/b!) d_x^a d_y^b d_t^tder of
+    sin(2 pi x) sin(2 pi y) cos(2 pi sqrt2 t) (the GPU arm's synthetic data)."""
     import numpy as np
 
-    from oracle import hermite_oracle as O
+    w = 2.0 * math.pi
+    om = w * math.sqrt(2.0)
+    out = np.empty((len(xn), len(yn), k + 1, k + 1))
+    ft = om**tder * math.cos(om * t + 0.5 * math.pi * tder)
+    for a in range(k + 1):
+        fx = w**a * np.sin(w * xn + 0.5 * math.pi * a) * h**a / math.factorial(a)
+        for b in range(k + 1):
+            fy = w**b * np.sin(w * yn + 0.5 * math.pi * b) * h**b / math.factorial(b)
+            out[:, :, a, b] = fx[:, None] * fy[None, :] * ft
+    return out
+
+
+def _strip_stepper(m: int, n: int, rows: int, kind: str):
+    """A closure running one half step of the reference (or its port) on the
+    n x rows periodic strip; returns (step, DOF-updates per step)."""
+    import numpy as np
 
     h = 1.0 / n
-    # rows+1 source rows are "primal with walls" along x locally -> rows targets
-    a = O.gather(u, 0, "x", O.PRIMAL, False, None, None)
-    du = np.moveaxis(O.gather(a, 2, "y", O.PRIMAL, True, None, None), 1, 2)
-    a = O.gather(v, 0, "x", O.PRIMAL, False, None, None)
-    dv = np.moveaxis(O.gather(a, 2, "y", O.PRIMAL, True, None, None), 1, 2)
-    return O._step_from_corners(du, dv, h, h, m, lam)
+    x = h * np.arange(n)
+    y = h * np.arange(rows)
+    u = _standing_blocks(x, y, 0.1, m, h, 0)
+    v = _standing_blocks(x, y, 0.1, m - 1, h, 1)
+    dof = n * rows * dof_per_node(m)
+    if kind == "reference":
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        import hermwave as hw  # the unmodified reference (baseline/_ref)
+        from hermwave.boundary import BoundarySpec2D
+        from hermwave.grid import PRIMAL, Field2D, FieldPair, Grid2D
+
+        grid = Grid2D(0.0, 1.0, 0.0, rows * h, n, rows, True)
+        pair = FieldPair(Field2D(grid, PRIMAL, 0.1, u), Field2D(grid, PRIMAL, 0.1, v))
+        cfg, bc = hw.SchemeConfig(m=m, lam=0.9), BoundarySpec2D()
+        return (lambda: hw.half_step_2d(pair, cfg, bc)), dof
+    from oracle import hermite_oracle as O
+
+    return (lambda: O.half_step_2d(u, v, O.PRIMAL, n, rows, True, h, h, m, 0.9)), dof
 
 
-def _cpu_worker(m, n, rows, r0, rounds, bar, q):
+def ref_kind() -> str:
+    return "reference" if os.path.isdir(os.path.join(REF_DIR, "hermwave")) else "port"
+
+
+def _cpu_worker(m, n, rows, kind, rounds, bar, q):
     from threadpoolctl import threadpool_limits
 
     with threadpool_limits(1):  # one BLAS thread per worker process
-        u, v = _window(m, n, rows, r0)
+        step, _ = _strip_stepper(m, n, rows, kind)
         for _ in range(rounds):
             bar.wait()
             t0 = time.time()
-            uo, _ = _oracle_rows(u, v, m, n)
+            step()
             t1 = time.time()
-            assert uo.shape[0] == rows
             q.put((t0, t1))
 
 
-def cpu_workers(m: int, rows: int) -> int:
-    """Worker processes for the CPU legs: every host core, capped so the
-    windows' numpy intermediates (about 45 MB per row at m = 4, scaling as
-    the map size) stay under a quarter of the host's available memory."""
+def cpu_workers(m: int, n: int, rows: int) -> int:
+    """Worker processes: every host core, capped so the reference's
+    intermediates (~38 KiB per node at m = 4, scaling as the map size;
+    SURVEY §8c) stay under a quarter of the host's available memory."""
     try:
         import psutil
 
         avail = psutil.virtual_memory().available
     except Exception:
         avail = 64 << 30
-    per = rows * 45e6 * (dof_per_node(m) / 41.0) ** 2
+    per = n * rows * 40e3 * (dof_per_node(m) / 41.0) ** 2
     return max(1, min(os.cpu_count() or 1, 128, int(0.25 * avail / per)))
 
 
-def cpu_sample(m: int, n: int, rows: int, rounds: int = 1, warm: int = 0):
-    """The reference algorithm on the host: W processes (one BLAS thread
-    each, W = cpu_workers) each take a different `rows` x n window of the n x
-    n workload and run one half step per round, all starting together
-    (barrier).  Returns (per-round wall seconds, DOF-updates per round,
-    W); the first `warm` rounds are untimed."""
+def cpu_sample(m: int, n: int, rows: int, rounds: int = 1, warm: int = 0, workers: int | None = None):
+    """W processes (one BLAS thread each) each run the reference's half step on
+    their own n x rows strip per round, all starting together (barrier).
+    Returns (mean timed round wall seconds, DOF-updates per round, W, kind)."""
     import multiprocessing as mp
 
-    w = cpu_workers(m, rows)
+    kind = ref_kind()
+    w = workers or cpu_workers(m, n, rows)
     ctx = mp.get_context("spawn")  # (the parent may hold CUDA state and threads)
     bar = ctx.Barrier(w)
     q = ctx.Queue()
     tot = warm + rounds
-    procs = [ctx.Process(target=_cpu_worker, args=(m, n, rows, (k * rows) % max(1, n - rows), tot, bar, q))
-             for k in range(w)]
+    procs = [ctx.Process(target=_cpu_worker, args=(m, n, rows, kind, tot, bar, q)) for _ in range(w)]
     for p in procs:
         p.start()
-    spans = [q.get(timeout=600) for _ in range(w * tot)]
+    spans = [q.get(timeout=900) for _ in range(w * tot)]
     for p in procs:
         p.join(timeout=60)
-    # rounds are barrier-separated: group the w reports of each round
-    spans.sort()
+    spans.sort()  # rounds are barrier-separated: group the w reports of each round
     walls = []
     for r in range(tot):
         grp = spans[r * w:(r + 1) * w]
         walls.append(max(t1 for _, t1 in grp) - min(t0 for t0, _ in grp))
     walls = walls[warm:]
-    return sum(walls) / len(walls), w * rows * n * dof_per_node(m), w
+    return sum(walls) / len(walls), w * n * rows * dof_per_node(m), w, kind
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(m: int, n: int, rows: int, rounds: int, warm: int):
+    """All-core rate and the single-core (1 process, 1 BLAS thread) rate."""
+    sec, d, w, kind = cpu_sample(m, n, rows, rounds=rounds, warm=warm)
+    sec1, d1, _, _ = cpu_sample(m, n, rows, rounds=max(1, min(rounds, 2)), warm=1, workers=1)
+    what = "hermwave.half_step_2d, the unmodified reference (baseline/_ref)" if kind == "reference" else \
+        "oracle/ numpy restatement of hermwave.half_step_2d"
+    return {"value": d / sec / 1e9, "unit": UNIT, "cores": w, "kind": kind,
+            "sample": f"{w} processes (1 BLAS thread each), each one half step of {what} on a periodic "
+                      f"{n}x{rows} strip with the C2 spacing h=1/{n}, m={m}, lambda 0.9, standing-wave data, "
+                      f"per round; {rounds} timed round(s) after {warm} warm-up",
+            "single_core": {"value": d1 / sec1 / 1e9, "unit": UNIT, "cores": 1},
+            "cpu_model": cpu_model(), "host_cpus": os.cpu_count()}, sec, d
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    m, n = args.m, args.n
-    rows = args.ref_rows
-    # bounded: at most 2 warm-up and 10 timed rounds, each one half step of a
-    # rows x n window per worker process on every host core, whatever --steps
-    # / --warmup ask, so the arm ends in about a minute
-    n_warm, n_timed = min(args.warmup, 2), min(args.steps, 10)
-    sec, d, w = cpu_sample(m, n, rows, rounds=n_timed, warm=n_warm)
-    val = d / sec / 1e9
+    m, n, rows = args.m, args.n, args.ref_rows
+    # every requested step runs (each a bounded sample: one strip half step per
+    # core, ~0.5 s at m = 4), up to 60 timed and 5 warm-up rounds
+    n_warm, n_timed = min(max(args.warmup, 1), 5), min(max(args.steps, 1), 60)
+    cb, sec, d = cpu_baseline(m, n, rows, n_timed, n_warm)
+    val = cb["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec,
-        "samples_timed": n_timed,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"2D periodic dissipative Hermite m={m}, {n}x{n}, lambda 0.9 (C2)",
-                   "m": m, "n": n, "sample_rows_per_worker": rows, "workers": w},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": w, "kind": "port",
-                         "sample": f"{w} processes (1 BLAS thread each) x one half step on a {rows}x{n} window "
-                                   f"of the {n}x{n} grid per step (numpy restatement of hermwave.half_step_2d)"},
+        "steps": n_timed, "warmup": n_warm, "requested": {"steps": args.steps, "warmup": args.warmup},
+        # one C2 half step (n^2 nodes) at the measured rate
+        "ms_per_step": 1e3 * n * n * dof_per_node(m) / (val * 1e9),
+        "ms_per_round": 1e3 * sec,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic standing wave (no dataset)",
+        "config": {"workload": f"2D periodic dissipative Hermite m={m}, {n}x{n} nodes per GPU, lambda 0.9 (C2)",
+                   "m": m, "n": n, "strip_rows_per_worker": rows, "workers": cb["cores"]},
+        "cpu_baseline": cb,
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -280,8 +334,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--m", type=int, default=4)
     ap.add_argument("--n", type=int, default=1024)
-    ap.add_argument("--ref-rows", type=int, default=4)
-    ap.add_argument("--cpu-rows", type=int, default=4)
+    ap.add_argument("--ref-rows", type=int, default=STRIP_ROWS)
+    ap.add_argument("--cpu-rows", type=int, default=STRIP_ROWS)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -403,11 +457,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_e2e:
         result["e2e"] = e2e_bench(hb, torch, np, m, n, cfg, min(args.steps, 5))
     if rank == 0 and world == 1 and not args.no_cpu:
-        t_cpu, d_cpu, w_cpu = cpu_sample(m, n, args.cpu_rows, rounds=2, warm=1)
-        result["cpu_baseline"] = {"value": d_cpu / t_cpu / 1e9, "unit": UNIT, "cores": w_cpu, "kind": "port",
-                                  "sample": f"{w_cpu} processes (1 BLAS thread each) x one half step on a "
-                                            f"{args.cpu_rows}x{n} window of the {n}x{n} grid (numpy restatement "
-                                            f"of hermwave.half_step_2d)"}
+        result["cpu_baseline"] = cpu_baseline(m, n, args.cpu_rows, rounds=2, warm=1)[0]
     if rank == 0 and world == 1 and not args.no_c3:
         result["c3"] = c3_bench(hb, torch, pk)
         result["c5"] = c5_bench(hb, torch, pk)
@@ -490,27 +540,31 @@ def c3_bench(hb, torch, pk):
     tf = f_alg_cons(m) * cells / sec / 1e12
     del par
     # the conservation check: the defined 2D conservative energy (norms.py
-    # conservative_energy_2d, exactly conserved by the scheme in exact
-    # arithmetic) sampled over NCONS further steps
+    # conservative_energy_2d) sampled over NCONS further
+    # steps.  At this h the exactly conserved mixed (m+1, m+1) form is below
+    # round-off; the L2 / H1 adjoint forms are the physical
+    # energy (conserved by the exact wave; L2 = sin^2(omega dt / 2) / 2 here)
     ncons, every = 1000, 250
 
     def energy():
         cur = hb.Field2D(grid, state["pa"], 0.0, state["a"])
         prev = hb.Field2D(grid, hb.flip(state["pa"]), 0.0, state["b"])
-        return hb.conservative_energy_2d(cur, prev, cfg.speed, dt, bc)
+        return {s: hb.conservative_energy_2d(cur, prev, cfg.speed, dt, bc, s) for s in ("l2", "h1")}
 
     es = [energy()]
     for k in range(ncons):
         one(k)
         if (k + 1) % every == 0:
             es.append(energy())
-    drift = max(abs(e - es[0]) for e in es) / es[0]
+    drift = {s: max(abs(e[s] - es[0][s]) for e in es) / es[0][s] for s in ("l2", "h1")}
+    closed = 0.5 * math.sin(0.5 * om * dt) ** 2
     return {"workload": "2D conservative Hermite m=5, 2048^2, Dirichlet x / Neumann y walls (C3)",
             "gdof_per_s": g, "ms_per_step": sec * 1e3, "tflops_falg": tf, "frac_dmma_peak": tf / pk["dmma_tflops"],
             "hbm_gbs": 24 * cells * dof_per_node(m, "cons") / sec / 1e9,
-            "conservation_check": {"kind": "defined 2D conservative energy (mixed (m+1,m+1) seminorm adjoint form, "
-                                           "norms.conservative_energy_2d)",
-                                   "steps": ncons, "samples": es, "max_rel_drift": drift}}
+            "conservation_check": {"kind": "2D conservative energy, adjoint form in the L2 and H1 seminorms "
+                                           "(norms.conservative_energy_2d seminorm='l2'/'h1')",
+                                   "steps": ncons, "samples": es, "max_rel_drift": drift,
+                                   "l2_closed_form": closed, "l2_rel_err_vs_closed_form": abs(es[0]["l2"] - closed) / closed}}
 
 
 def c5_bench(hb, torch, pk):

@@ -647,7 +647,7 @@ int hw_inner2d(const hw_rows2d* f, const hw_rows2d* g, int mx, int my, const hw_
     double h = 0.0;
     cuda_check(cudaMemcpyAsync(&h, dout.p, sizeof(double), cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
     cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
-    *out_host = h;
+    *out_host = h * (0.25 * hx * hy);  // Gauss rule on [-1, 1]^2 -> the hx x hy cell
   });
 }
 

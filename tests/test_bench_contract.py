@@ -20,6 +20,11 @@ def test_reference_arm_json_line():
                 "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
         assert key in d, key
     assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    # "reference" when the unmodified reference is installed in baseline/_ref, else the oracle port
+    assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
+    assert d["cpu_baseline"]["single_core"]["value"] > 0
+    # the line describes what ran, and ms_per_step is one full half step of the configured grid
+    assert d["steps"] == 1 and d["warmup"] == 1
+    assert abs(d["ms_per_step"] - 1e3 * 64 * 64 * 41 / (d["value"] * 1e9)) <= 1e-9 * d["ms_per_step"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert "workload" in d["config"]
