@@ -506,7 +506,8 @@ static double cell_quadrature_2d(const hw_rows2d* src, int mx, int my, const hw_
   cuda_check(cudaMemcpy(gx.data(), gauss_x, npts * sizeof(double), cudaMemcpyDefault), "copy gauss x");
   cuda_check(cudaMemcpy(gw.data(), gauss_w, npts * sizeof(double), cudaMemcpyDefault), "copy gauss w");
   const std::vector<double> ex = deriv_eval_matrix(mx, dx, hx, gx), ey = deriv_eval_matrix(my, dy, hy, gx);
-  const int64_t ncell = g.ntx * g.nty;
+  const int64_t ncell = g.ntrows * g.nty;
+  if (ncell == 0) return 0.0;
   const int64_t nblk = (ncell + kRedThreads - 1) / kRedThreads;
   DevBuf dex, dey, dgx, dgw, dpart;
   cuda_check(cudaMalloc(&dex.p, ex.size() * 8), "cudaMalloc");
@@ -525,6 +526,8 @@ static double cell_quadrature_2d(const hw_rows2d* src, int mx, int my, const hw_
   a.ny = g.ny;
   a.ntx = g.ntx;
   a.nty = g.nty;
+  a.trow0 = g.trow0;
+  a.ntrows = g.ntrows;
   a.off = g.off;
   a.periodic = g.periodic;
   a.kxl = g.periodic ? 0 : geom->bcx.left_kind;

@@ -33,6 +33,7 @@ __global__ void sum_partials_kernel(const double* part, int64_t n, double* out) 
 struct L2Err2DArgs {
   Rows f;
   int64_t nx, ny, ntx, nty;
+  int64_t trow0, ntrows;  // target (cell) rows reduced: [trow0, trow0 + ntrows) (slabs)
   int off, periodic;
   int kxl, kxh, kyl, kyh;
   double gxl, gxh, gyl, gyh;
@@ -42,7 +43,7 @@ struct L2Err2DArgs {
   const double* gw;   // Gauss weights
   const double* gx;   // Gauss nodes on [-1,1]
   int exact_kind;
-  const double* exact;  // [ci][cj][p][q]
+  const double* exact;  // [ci - trow0][cj][p][q]
   double prm[4];
   double x0, y0, hx, hy, coff;  // target node coordinates x0 + hx (i + coff)
   double* part;
@@ -58,11 +59,11 @@ __device__ inline double exact_builtin(int kind, const double* prm, double x, do
 // gives the squared seminorm sum of the 2D energy (hw_seminorm2d).
 __global__ void l2err2d_kernel(L2Err2DArgs a) {
   __shared__ double sh[kRedThreads];
-  const int64_t ncell = a.ntx * a.nty;
+  const int64_t ncell = a.ntrows * a.nty;
   const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double local = 0.0;
   if (cell < ncell) {
-    const int64_t ti = cell / a.nty, tj = cell - ti * a.nty;
+    const int64_t tl = cell / a.nty, tj = cell - tl * a.nty, ti = a.trow0 + tl;
     const int mx = a.mx, my = a.my, wx = mx + 1, wy = my + 1, P = wx * wy;
     const RowRef r0 = resolve_row(a.f, ti + a.off, a.nx, a.ny * P, a.periodic, a.kxl, a.kxh, a.gxl, a.gxh);
     const RowRef r1 = resolve_row(a.f, ti + a.off + 1, a.nx, a.ny * P, a.periodic, a.kxl, a.kxh, a.gxl, a.gxh);
@@ -93,7 +94,7 @@ __global__ void l2err2d_kernel(L2Err2DArgs a) {
         for (int e = 0; e < 2 * wx; ++e) val = fma(__ldg(a.ex + p * 2 * wx + e), T[e], val);
         double ex;
         if (a.exact_kind == 0) {
-          ex = a.exact[((ti * a.nty + tj) * a.npts + p) * a.npts + q];
+          ex = a.exact[((tl * a.nty + tj) * a.npts + p) * a.npts + q];
         } else if (a.exact_kind == 3) {  // seminorms: the derivative interpolant alone
           ex = 0.0;
         } else {

@@ -159,7 +159,8 @@ def test_device_energy_2d_matches_oracle(m, par, kind, seminorm):
                                     speed, dt, bc, seminorm)
     want = O.cons_energy_2d(a, b, par, per, h, h, speed, dt, bx, by, seminorm)
     # Gauss vs closed-form Gram, interpolants amplified by cond(M_mu) at high m
-    assert got == pytest.approx(want, rel={8: 1e-9}.get(m, 1e-12))
+    # (and by the 17!/8! derivative factors of the mixed (9, 9) seminorm at m = 8)
+    assert got == pytest.approx(want, rel={8: 1e-8 if seminorm == "mixed" else 1e-9}.get(m, 1e-12))
 
 
 @pytest.mark.gpu
