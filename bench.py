@@ -11,11 +11,15 @@ coefficient advanced one half step: (m+1)^2 + m^2 = 41 per node.
 
 N > 1 (torchrun, one rank per GPU): weak scaling, each rank owns a
 1024 x 1024 slab of a (1024 N) x 1024 periodic grid and exchanges one node
-row per half step with its ring neighbour (torch.distributed P2P over NCCL).
+row per half step with its ring neighbour (torch.distributed P2P over NCCL),
+so the per-N values are the same per-GPU workload as N = 1.
 
-Extra keys beside the contract's: "c3" (conservative m=5, 2048^2,
-Dirichlet/Neumann walls — BASELINE configs[2]) and "sweep" (dissipative
-m=2..8 at ~2^30 DOF per level — configs[3]), both device resident.
+Extra keys beside the contract's: "c5" at every N (BASELINE configs[4]:
+m=6, strong scaling at 8192^2 and 16384^2 (N >= 4), weak at 2048N x 16384,
+through the slab ring), and at N = 1 "c3" (conservative m=5, 2048^2,
+Dirichlet/Neumann walls — configs[2], with its energy drift) and "sweep"
+(dissipative m=2..8 at ~2^30 DOF per level — configs[3]), all device
+resident.  --config c5 makes C5's weak-scaling slab the top-level workload.
 """
 
 from __future__ import annotations
@@ -326,12 +330,67 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def slab_run(hb, torch, dist, ring, m, steps, warmup, stream, events=True):
+    """Device-resident dissipative half steps of this rank's slab of ring.grid
+    (standing wave from t0 = 0.1), timed with CUDA events on the
+    launching stream between barriers; returns (ms total, mean kernel ms)."""
+    grid = ring.grid
+    cfg = hb.SchemeConfig(m=m, lam=0.9)
+    w = 2.0 * math.pi  # u = sin(2 pi x) sin(2 pi y) cos(2 pi sqrt2 t) (h = 1/ny, y extent 1)
+    om = w * math.sqrt(2.0)
+
+    def init(parity, k, tder):
+        return hb.standing_wave_on_grid(grid, parity, 0.1, k, k, w, w, om, tder=tder,
+                                        rows=(ring.row0, ring.nrows(parity)))
+
+    u, v = init(hb.PRIMAL, m, 0), init(hb.PRIMAL, m - 1, 1)
+    bufs = [(u, v), (torch.empty_like(u), torch.empty_like(v))]
+    bc = hb.BoundarySpec2D()
+    parity = hb.PRIMAL
+
+    def step(i, par):
+        ring.diss2d_step(*bufs[i % 2], *bufs[(i + 1) % 2], par, m, cfg, bc, stream.cuda_stream)
+
+    for i in range(warmup):
+        step(i, parity)
+        parity = hb.flip(parity)
+    torch.cuda.synchronize()
+    if ring.world > 1:
+        dist.barrier()
+    k_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start.record(stream)
+    for i in range(steps):
+        ring.kernel_events = k_ev[i] if events else None
+        step(warmup + i, parity)
+        parity = hb.flip(parity)
+    stop.record(stream)
+    torch.cuda.synchronize()
+    ring.kernel_events = None
+    if ring.world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(stop)
+    kern_ms = sum(a.elapsed_time(b) for a, b in k_ev) / steps if events else float("nan")
+    if ring.world > 1:  # the job's time is the slowest rank's
+        t = torch.tensor([ms, kern_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, kern_ms = float(t[0]), float(t[1])
+    del u, v, bufs
+    torch.cuda.empty_cache()
+    return ms, kern_ms
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c5"],
+                    help="top-level workload: c2 (default; weak-scaled 1024^2 per GPU at N > 1) or c5 "
+                         "(m=6, 2048 N x 16384 periodic, 2048 x 16384 per GPU: BASELINE configs[4] weak scaling)")
     ap.add_argument("--m", type=int, default=4)
     ap.add_argument("--n", type=int, default=1024)
     ap.add_argument("--ref-rows", type=int, default=STRIP_ROWS)
@@ -340,6 +399,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c3", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -348,6 +408,11 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if world > 1:
+        # NCCL's init lines (ranks, rings/NVLS, transports) to stderr: stdout keeps the one JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
     import numpy as np
     import torch
@@ -357,77 +422,43 @@ def main():
     from paper_1802_05246_b200.slab import SlabRing
 
     torch.cuda.set_device(local)
+    comm = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    m, n = args.m, args.n
-    lam = 0.9
-    nx_glob = n * world
-    grid = hb.Grid2D(0.0, float(world), 0.0, 1.0, nx_glob, n, True)  # h = 1/n on both axes
-    cfg = hb.SchemeConfig(m=m, lam=lam)
-    t0 = 0.1
-    w = 2.0 * math.pi
-    om = w * math.sqrt(2.0)
-    ring = SlabRing(grid, rank, world)
-
-    def init(parity, kx, tder):
-        sub = ring.local_grid(parity)
-        return hb.standing_wave_on_grid(sub, parity, t0, kx, kx, w, w, om, tder=tder)
-
-    u = init(hb.PRIMAL, m, 0)
-    v = init(hb.PRIMAL, m - 1, 1)
-    ud = torch.empty_like(u)
-    vd = torch.empty_like(v)
+        chk = torch.ones(1, device="cuda")
+        dist.all_reduce(chk)
+        comm = {"backend": dist.get_backend(), "world": dist.get_world_size(),
+                "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version()),
+                "allreduce_check": float(chk) == float(world)}
     stream = torch.cuda.current_stream()
-
-    def step(src, dst, parity):
-        ring.diss2d_step(src[0], src[1], dst[0], dst[1], parity, m, cfg, hb.BoundarySpec2D(), stream.cuda_stream)
-
-    bufs = [(u, v), (ud, vd)]
-    parity = hb.PRIMAL
-    for i in range(args.warmup):
-        step(bufs[i % 2], bufs[(i + 1) % 2], parity)
-        parity = hb.flip(parity)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    k_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    start = torch.cuda.Event(enable_timing=True)
-    stop = torch.cuda.Event(enable_timing=True)
+    pk = peaks()
+    if args.config == "c5":
+        m, ny, rows_per = 6, 16384, 2048
+        workload = f"C5 (BASELINE configs[4]) weak scaling: 2D periodic dissipative Hermite m=6, " \
+                   f"{rows_per * world}x{ny} nodes ({rows_per}x{ny} per GPU), lambda 0.9"
+    else:
+        m, ny, rows_per = args.m, args.n, args.n
+        workload = f"2D periodic dissipative Hermite m={m}, {rows_per}x{ny} nodes per GPU, lambda 0.9 (C2)"
+    nx_glob = rows_per * world
+    grid = hb.Grid2D(0.0, nx_glob / ny, 0.0, 1.0, nx_glob, ny, True)  # h = 1/ny on both axes
+    ring = SlabRing(grid, rank, world)
+    ms, kern_ms = 0.0, 0.0
     with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        start.record()
-        for i in range(args.steps):
-            j = args.warmup + i
-            ring.kernel_events = k_ev[i]
-            step(bufs[j % 2], bufs[(j + 1) % 2], parity)
-            parity = hb.flip(parity)
-        stop.record()
-        torch.cuda.synchronize()
-    ring.kernel_events = None
-    if world > 1:
-        dist.barrier()
-    ms = start.elapsed_time(stop)
-    kern_ms = sum(a.elapsed_time(b) for a, b in k_ev) / args.steps
-    if world > 1:
-        t = torch.tensor([ms, kern_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, kern_ms = float(t[0]), float(t[1])
+        ms, kern_ms = slab_run(hb, torch, dist, ring, m, args.steps, args.warmup, stream)
     sec = ms / 1e3
-    cells_total = nx_glob * n
-    dofs = cells_total * dof_per_node(m) * args.steps
+    dofs = nx_glob * ny * dof_per_node(m) * args.steps
     value = dofs / sec / 1e9
 
     # roofline of the dominant kernel (cellmap_kernel<m, diss>): FP64 tensor
     # pipe (DMMA).  achieved = SURVEY §8d's canonical flops per cell x cells /
     # kernel time; "dense"/"issued" are what this kernel's cell maps execute.
-    pk = peaks()
-    cells_rank = ring.nrows * n
+    cells_rank = ring.nrows(hb.PRIMAL) * ny
     ksec = kern_ms / 1e3
     achieved = f_alg_diss(m) * cells_rank / ksec / 1e12
     dense, issued = cellmap_flops(m)
     bytes_alg = 16 * cells_rank * dof_per_node(m)
     ncu = load_json(os.path.join(ROOT, "profiles", "ncu_summary.json")) or {}
-    traffic = (ncu.get("launches", {}).get(f"diss_m{m}_n{n}") or {}).get("dram_bytes")
+    traffic = (ncu.get("launches", {}).get(f"diss_m{m}_n{ny}") or {}).get("dram_bytes")
     roofline = {
         "bound": "tensor", "achieved": achieved, "peak": pk["dmma_tflops"], "unit": "TFLOP/s",
         "frac": achieved / pk["dmma_tflops"], "traffic": traffic,
@@ -443,30 +474,118 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic standing wave (no dataset)",
-        "config": {"workload": f"2D periodic dissipative Hermite m={m}, {n}x{n} nodes per GPU, lambda 0.9 (C2)",
-                   "m": m, "nodes_per_gpu": [ring.nrows, n], "global_nodes": [nx_glob, n],
-                   "dof_per_node": dof_per_node(m),
+        "config": {"workload": workload, "m": m, "nodes_per_gpu": [ring.nrows(hb.PRIMAL), ny],
+                   "global_nodes": [nx_glob, ny], "dof_per_node": dof_per_node(m),
                    "l2": "inputs larger than L2 (u+v = %.0f MB per parity, L2 126 MB); no flush" % (
                        cells_rank * dof_per_node(m) * 8 / 1e6),
-                   "parallelism": f"slab{world}" if world > 1 else "single"},
+                   "parallelism": f"slab{world} (x rows, one-row NCCL halo per half step)" if world > 1
+                   else "single"},
         "roofline": roofline,
+        # one cell-map launch per half step (interior + halo row: two at N > 1)
         "gpu_launches": args.steps * (1 if world == 1 else 2),
         "clocks": clk.summary(),
     }
+    if comm is not None:
+        result["comm"] = comm
 
-    if rank == 0 and world == 1 and not args.no_e2e:
-        result["e2e"] = e2e_bench(hb, torch, np, m, n, cfg, min(args.steps, 5))
+    if not args.no_e2e:
+        if world == 1:
+            e2e = e2e_bench(hb, torch, np, m, ny, hb.SchemeConfig(m=m, lam=0.9), min(args.steps, 5))
+        else:
+            e2e = e2e_slab(hb, torch, dist, ring, m, min(args.steps, 5), stream)
+        if rank == 0:
+            result["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu:
-        result["cpu_baseline"] = cpu_baseline(m, n, args.cpu_rows, rounds=2, warm=1)[0]
+        result["cpu_baseline"] = cpu_baseline(m, ny, args.cpu_rows, rounds=2, warm=1)[0]
     if rank == 0 and world == 1 and not args.no_c3:
         result["c3"] = c3_bench(hb, torch, pk)
-        result["c5"] = c5_bench(hb, torch, pk)
+    if not args.no_c5:
+        c5 = c5_scaling(hb, torch, dist, rank, world, stream, pk)
+        if rank == 0:
+            result["c5"] = c5
     if rank == 0 and world == 1 and not args.no_sweep:
         result["sweep"] = sweep(hb, torch, pk)
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def c5_scaling(hb, torch, dist, rank, world, stream, pk):
+    """BASELINE configs[4] (C5): 2D periodic dissipative m = 6 through the slab
+    ring at this run's N: strong scaling at 8192^2 (45.6 GB per level, fits one
+    GPU) and 16384^2 (182.5 GB per level: N >= 4), weak scaling at 2048 N x
+    16384 (2048 x 16384 per GPU).  Device resident, 2 warm-up + 4 timed half
+    steps each, max over ranks."""
+    from paper_1802_05246_b200.slab import SlabRing
+
+    m = 6
+    cases = [("strong_8192", 8192, 8192), ("weak_2048Nx16384", 2048 * world, 16384)]
+    if world >= 4:
+        cases.append(("strong_16384", 16384, 16384))
+    out = {"workload": "C5 (BASELINE configs[4]): 2D periodic dissipative Hermite m=6, lambda 0.9, standing wave; "
+                       "strong scaling at 8192^2 (N=1/2/4/8) and 16384^2 (N=4/8), weak at 2048N x 16384",
+           "n_gpus": world}
+    for name, nx, ny in cases:
+        grid = hb.Grid2D(0.0, nx / ny, 0.0, 1.0, nx, ny, True)
+        ring = SlabRing(grid, rank, world)
+        steps = 4
+        ms, kern_ms = slab_run(hb, torch, dist, ring, m, steps, 2, stream)
+        sec = ms / 1e3 / steps
+        tf = f_alg_diss(m) * nx * ny / sec / 1e12
+        out[name] = {"global_nodes": [nx, ny], "nodes_per_gpu": [ring.nrows(hb.PRIMAL), ny],
+                     "gdof_per_s": nx * ny * dof_per_node(m) / sec / 1e9, "ms_per_step": sec * 1e3,
+                     "kernel_ms_per_step": kern_ms, "tflops_falg": tf,
+                     "frac_dmma_peak_per_gpu": tf / world / pk["dmma_tflops"], "steps": steps}
+    return out
+
+
+def e2e_slab(hb, torch, dist, ring, m, steps, stream):
+    """End to end at N GPUs through the public slab API: every step each rank
+    uploads its slab's (u, v) from pinned host memory, runs
+    SlabRing.diss2d_step (NCCL halo + kernels) and reads the new state back;
+    host wall clock, max over ranks."""
+    grid = ring.grid
+    cfg = hb.SchemeConfig(m=m, lam=0.9)
+    w = 2.0 * math.pi
+    shp_u = ring.local_shape(hb.PRIMAL, m, m)
+    shp_v = ring.local_shape(hb.PRIMAL, m - 1, m - 1)
+    hu = torch.empty(shp_u, dtype=torch.float64, pin_memory=True)
+    hv = torch.empty(shp_v, dtype=torch.float64, pin_memory=True)
+    hu.copy_(hb.standing_wave_on_grid(grid, hb.PRIMAL, 0.1, m, m, w, w, w * math.sqrt(2.0),
+                                      rows=(ring.row0, ring.nrows(hb.PRIMAL))))
+    hv.copy_(hb.standing_wave_on_grid(grid, hb.PRIMAL, 0.1, m - 1, m - 1, w, w, w * math.sqrt(2.0), tder=1,
+                                      rows=(ring.row0, ring.nrows(hb.PRIMAL))))
+    du, dv = torch.empty(shp_u, dtype=torch.float64, device="cuda"), torch.empty(shp_v, dtype=torch.float64,
+                                                                                 device="cuda")
+    ou, ov = torch.empty_like(du), torch.empty_like(dv)
+    bc = hb.BoundarySpec2D()
+
+    def one(par):
+        du.copy_(hu, non_blocking=True)
+        dv.copy_(hv, non_blocking=True)
+        ring.diss2d_step(du, dv, ou, ov, par, m, cfg, bc, stream.cuda_stream)
+        hu.copy_(ou, non_blocking=True)
+        hv.copy_(ov, non_blocking=True)
+
+    par = hb.PRIMAL
+    one(par)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        par = hb.flip(par)
+        one(par)
+    torch.cuda.synchronize()
+    sec = time.perf_counter() - t0
+    t = torch.tensor([sec], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    sec = float(t[0])
+    nbytes = (hu.numel() + hv.numel()) * 8
+    return {"value": grid.nx * grid.ny * dof_per_node(m) * steps / sec / 1e9, "unit": UNIT,
+            "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+            "api": "paper_1802_05246_b200.slab.SlabRing.diss2d_step (pinned host slabs, per rank)",
+            "steps": steps, "timer": "host wall clock around the steps, max over ranks"}
 
 
 def e2e_bench(hb, torch, np, m, n, cfg, steps):
@@ -565,36 +684,6 @@ def c3_bench(hb, torch, pk):
                                            "(norms.conservative_energy_2d seminorm='l2'/'h1')",
                                    "steps": ncons, "samples": es, "max_rel_drift": drift,
                                    "l2_closed_form": closed, "l2_rel_err_vs_closed_form": abs(es[0]["l2"] - closed) / closed}}
-
-
-def c5_bench(hb, torch, pk):
-    """Config C5 at its single-GPU size: dissipative m = 6 on 8192^2 (45.6 GB
-    per level), the strong-scaling base of the 1/2/4/8-GPU runs."""
-    from paper_1802_05246_b200.stepping import diss2d_into
-
-    m, n = 6, 8192
-    grid = hb.Grid2D(0.0, 1.0, 0.0, 1.0, n, n, True)
-    cfg = hb.SchemeConfig(m=m, lam=0.9)
-    w = 2.0 * math.pi
-    u = hb.standing_wave_on_grid(grid, hb.PRIMAL, 0.1, m, m, w, w, w * math.sqrt(2.0))
-    v = hb.standing_wave_on_grid(grid, hb.PRIMAL, 0.1, m - 1, m - 1, w, w, w * math.sqrt(2.0), tder=1)
-    bufs = [(u, v), (torch.empty_like(u), torch.empty_like(v))]
-    st = {"par": hb.PRIMAL}
-
-    def one(i):
-        diss2d_into(*bufs[i % 2], *bufs[(i + 1) % 2], grid, st["par"], m, cfg, hb.BoundarySpec2D())
-        st["par"] = hb.flip(st["par"])
-
-    for i in range(2):
-        one(i)
-    torch.cuda.synchronize()
-    sec = _time_steps(torch, lambda i: one(i + 2), 4)
-    tf = f_alg_diss(m) * n * n / sec / 1e12
-    del u, v, bufs
-    torch.cuda.empty_cache()
-    return {"workload": "2D periodic dissipative Hermite m=6, 8192^2 (C5 single-GPU size)",
-            "gdof_per_s": n * n * dof_per_node(m) / sec / 1e9, "ms_per_step": sec * 1e3, "tflops_falg": tf,
-            "frac_dmma_peak": tf / pk["dmma_tflops"]}
 
 
 def sweep(hb, torch, pk):

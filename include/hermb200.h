@@ -234,9 +234,10 @@ int hw_count_nonfinite(const double* a, int64_t n, int64_t* nonfinite_host,
 /*
  * driver.py:241-256 planewave_data on the device: out[i][j][k][l] scaled
  * blocks of sin(w(x+y+sqrt2 t)) (tder = 0) or its time derivative (tder = 1)
- * at nodes x_i = x0 + hx*(i+off), y_j = y0 + hy*(j+off).
+ * at nodes x_i = x0 + hx*(row0+i+off), y_j = y0 + hy*(j+off), i < nx local
+ * rows of a slab starting at global row row0 (0 for a whole grid).
  */
-int hw_init_planewave2d(double* out, int64_t nx, int64_t ny, int kx, int ky,
+int hw_init_planewave2d(double* out, int64_t nx, int64_t ny, int64_t row0, int kx, int ky,
                         double x0, double y0, double off, double t,
                         double kappa, double hx, double hy, int tder,
                         void* stream);
@@ -246,7 +247,7 @@ int hw_init_planewave2d(double* out, int64_t nx, int64_t ny, int kx, int ky,
  * (tder = 1) as scaled blocks; with trig shift phases (px, py) so that
  * sin(pi x)cos(pi y) style products are expressible: sin(ax x + px) ...
  */
-int hw_init_standing2d(double* out, int64_t nx, int64_t ny, int kx, int ky,
+int hw_init_standing2d(double* out, int64_t nx, int64_t ny, int64_t row0, int kx, int ky,
                        double x0, double y0, double off, double t, double ax,
                        double ay, double px, double py, double om, double hx,
                        double hy, int tder, void* stream);

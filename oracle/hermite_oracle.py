@@ -371,6 +371,19 @@ def bootstrap_2d(g0, g1, parity, periodic, hx, hy, m, lam, speed=1.0, bcx=PERIOD
 
 # ----------------------------------------------------------------- diagnostics.py
 
+def l2_cells_2d(c, cx, cy, hx, hy, exact, npts):
+    """Per-cell (hx hy / 4) sum_pq w_p w_q (I u - exact)^2 from the cells' interpolant
+    coefficients c (..., 2mx+2, 2my+2) and centres cx, cy (diagnostics.py:118-135)."""
+    xg, wg = np.polynomial.legendre.leggauss(npts)
+    vx = np.vander(0.5 * xg, c.shape[-2], increasing=True)
+    vy = np.vander(0.5 * xg, c.shape[-1], increasing=True)
+    vals = np.einsum("ijab,pa,qb->ijpq", c, vx, vy, optimize=True)
+    x = cx[:, None] + 0.5 * hx * xg[None, :]
+    y = cy[:, None] + 0.5 * hy * xg[None, :]
+    diff = vals - exact(x[:, None, :, None], y[None, :, None, :])
+    return np.sum(diff * diff * (wg[:, None] * wg[None, :]), axis=(2, 3)) * (0.25 * hx * hy)
+
+
 def l2_error_2d(values, parity, nx, ny, periodic, x_left, y_left, hx, hy, exact, npts=None,
                 bcx=PERIODIC_BC, bcy=PERIODIC_BC):
     """diagnostics.py:118-135."""
@@ -544,20 +557,29 @@ def _cons_apply_2d(values, parity, periodic, hx, hy, m, speed, dt, bcx=PERIODIC_
     return 2.0 * np.einsum("klab,...ab->...kl", wt, c, optimize=True)
 
 
+def inner_cells_2d(cx, cy, hx, hy, dx, dy):
+    """Per-cell int int (d_x^dx d_y^dy p)(d_x^dx d_y^dy q) of cell polynomials with
+    coefficient arrays cx, cy (..., 2mx+2, 2my+2) in the cell variables, exactly
+    (monomial Gram)."""
+    nxc, nyc = cx.shape[-2] - dx, cx.shape[-1] - dy
+    if nxc <= 0 or nyc <= 0:
+        return np.zeros(cx.shape[:-2])
+    fx = np.array([math.factorial(a + dx) / math.factorial(a) for a in range(nxc)]) / hx**dx
+    fy = np.array([math.factorial(b + dy) / math.factorial(b) for b in range(nyc)]) / hy**dy
+    dX = cx[..., dx:, dy:] * fx[:, None] * fy[None, :]
+    dY = cy[..., dx:, dy:] * fx[:, None] * fy[None, :]
+    return hx * hy * np.einsum("ijab,ac,ijcd,bd->ij", dX, _monomial_gram(nxc), dY, _monomial_gram(nyc))
+
+
 def inner_2d(x, y, parity, periodic, hx, hy, dx, dy, bcx=PERIODIC_BC, bcy=PERIODIC_BC):
     """sum over the field's cells of w_cell * int int (d_x^dx d_y^dy I x)(d_x^dx d_y^dy I y),
     integrated in closed form (monomial Gram); w_cell = 1/2 per axis on which the
     cell straddles a wall (ghost-padded dual cells), else 1."""
     cx = interp_2d(corner_data(x, parity, periodic, bcx, bcy))
     cy = cx if y is x else interp_2d(corner_data(y, parity, periodic, bcx, bcy))
-    nxc, nyc = cx.shape[-2] - dx, cx.shape[-1] - dy
-    if nxc <= 0 or nyc <= 0:
+    per_cell = inner_cells_2d(cx, cy, hx, hy, dx, dy)
+    if per_cell.ndim < 2:
         return 0.0
-    fx = np.array([math.factorial(a + dx) / math.factorial(a) for a in range(nxc)]) / hx**dx
-    fy = np.array([math.factorial(b + dy) / math.factorial(b) for b in range(nyc)]) / hy**dy
-    dX = cx[..., dx:, dy:] * fx[:, None] * fy[None, :]
-    dY = cy[..., dx:, dy:] * fx[:, None] * fy[None, :]
-    per_cell = hx * hy * np.einsum("ijab,ac,ijcd,bd->ij", dX, _monomial_gram(nxc), dY, _monomial_gram(nyc))
     wx = np.ones(per_cell.shape[0])
     wy = np.ones(per_cell.shape[1])
     if not periodic and parity == DUAL:

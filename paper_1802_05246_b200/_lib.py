@@ -100,8 +100,8 @@ def _declare(lib):
                                C.POINTER(_D), _P]),
         "hw_inner2d": (_I, [C.POINTER(Rows2D), C.POINTER(Rows2D), _I, _I, C.POINTER(Geom2D), _D, _D, _I, _I, _I,
                             _P, _P, _I, C.POINTER(_D), _P]),
-        "hw_init_planewave2d": (_I, [_P, _L, _L, _I, _I, _D, _D, _D, _D, _D, _D, _D, _I, _P]),
-        "hw_init_standing2d": (_I, [_P, _L, _L, _I, _I, _D, _D, _D, _D, _D, _D, _D, _D, _D,
+        "hw_init_planewave2d": (_I, [_P, _L, _L, _L, _I, _I, _D, _D, _D, _D, _D, _D, _D, _I, _P]),
+        "hw_init_standing2d": (_I, [_P, _L, _L, _L, _I, _I, _D, _D, _D, _D, _D, _D, _D, _D, _D,
                                     _D, _D, _I, _P]),
     }
     for name, (res, args) in sig.items():

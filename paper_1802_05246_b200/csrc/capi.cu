@@ -990,15 +990,18 @@ static void launch_init(const Init2DArgs& a, cudaStream_t st) {
   cuda_check(cudaGetLastError(), "init2d launch");
 }
 
-int hw_init_planewave2d(double* out, int64_t nx, int64_t ny, int kx, int ky, double x0, double y0, double off,
+int hw_init_planewave2d(double* out, int64_t nx, int64_t ny, int64_t row0, int kx, int ky, double x0, double y0,
+                        double off,
                         double t, double kappa, double hx, double hy, int tder, void* stream) {
   return guard([&] {
     HW_CHECK(out, "null output");
     Init2DArgs a;
     std::memset(&a, 0, sizeof(a));
     a.out = out;
+    HW_CHECK(row0 >= 0, "row offset must be nonnegative");
     a.nx = nx;
     a.ny = ny;
+    a.row0 = row0;
     a.kx = kx;
     a.ky = ky;
     a.x0 = x0;
@@ -1014,7 +1017,8 @@ int hw_init_planewave2d(double* out, int64_t nx, int64_t ny, int kx, int ky, dou
   });
 }
 
-int hw_init_standing2d(double* out, int64_t nx, int64_t ny, int kx, int ky, double x0, double y0, double off,
+int hw_init_standing2d(double* out, int64_t nx, int64_t ny, int64_t row0, int kx, int ky, double x0, double y0,
+                       double off,
                        double t, double ax, double ay, double px, double py, double om, double hx, double hy,
                        int tder, void* stream) {
   return guard([&] {
@@ -1022,8 +1026,10 @@ int hw_init_standing2d(double* out, int64_t nx, int64_t ny, int kx, int ky, doub
     Init2DArgs a;
     std::memset(&a, 0, sizeof(a));
     a.out = out;
+    HW_CHECK(row0 >= 0, "row offset must be nonnegative");
     a.nx = nx;
     a.ny = ny;
+    a.row0 = row0;
     a.kx = kx;
     a.ky = ky;
     a.x0 = x0;

@@ -322,6 +322,7 @@ __global__ void nonfinite_kernel(const double* x, int64_t n, unsigned long long*
 struct Init2DArgs {
   double* out;
   int64_t nx, ny;
+  int64_t row0;  // global index of local row 0 (slabs): x = x0 + hx (row0 + i + off)
   int kx, ky;
   double x0, y0, off, t, hx, hy;
   int kind;  // 1 plane wave, 2 standing wave
@@ -334,7 +335,7 @@ __global__ void init2d_kernel(Init2DArgs a) {
   const int64_t node = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (node >= a.nx * a.ny) return;
   const int64_t i = node / a.ny, j = node - i * a.ny;
-  const double x = a.x0 + a.hx * ((double)i + a.off);
+  const double x = a.x0 + a.hx * ((double)(a.row0 + i) + a.off);
   const double y = a.y0 + a.hy * ((double)j + a.off);
   const int wx = a.kx + 1, wy = a.ky + 1;
   double* o = a.out + node * wx * wy;

@@ -66,29 +66,27 @@ class StandingWave2D:
         return 2, (self.ax, self.ay, self.om, self.t)
 
 
-def l2_error_field_2d(field: Field2D, exact, bc: BoundarySpec2D, npts: int | None = None) -> float:
-    """L2 error of the global tensor interpolant (diagnostics.py:118-135).
-
-    Like the reference, cells are the targets of the field's own corner
-    gather (no clipping in 2D)."""
-    mx, my = field.orders
-    npts = npts or default_npts(max(mx, my))
-    grid = field.grid
-    g = geom2d(grid, field.parity, bc)
+def _l2_sum_2d(f, grid, parity: str, orders, exact, bc: BoundarySpec2D, npts: int, trow0: int = 0,
+               ntrows: int = -1, rows=None) -> float:
+    """sum over the cells [trow0, trow0 + ntrows) of the field's corner gather of
+    (hx hy / 4) sum_pq w_p w_q (I f - exact)^2 (hw_l2err2d; the square of
+    diagnostics.py:118-135's result when the window is the whole grid)."""
+    mx, my = orders
+    g = geom2d(grid, parity, bc, trow0, ntrows)
     xg, wg = gauss_rule(npts)
-    st = Staging(field.values)
-    f = st.to_dev(field.values)
     params = (C.c_double * 4)(0.0, 0.0, 0.0, 0.0)
     ex_dev = None
     form = getattr(exact, "device_form", None)
+    st = Staging(f)
     if form is not None:
         kind, prm = form
         for i, p in enumerate(prm):
             params[i] = float(p)
     else:
         kind = 0
-        cx = grid.axis(0).nodes(flip(field.parity))
-        cy = grid.axis(1).nodes(flip(field.parity))
+        cx = grid.axis(0).nodes(flip(parity))
+        cx = cx[trow0: (len(cx) if ntrows < 0 else trow0 + ntrows)]
+        cy = grid.axis(1).nodes(flip(parity))
         x = cx[:, None] + 0.5 * grid.hx * xg[None, :]
         y = cy[:, None] + 0.5 * grid.hy * xg[None, :]
         ex = np.broadcast_to(exact(x[:, None, :, None], y[None, :, None, :]),
@@ -97,12 +95,25 @@ def l2_error_field_2d(field: Field2D, exact, bc: BoundarySpec2D, npts: int | Non
     gx = np.ascontiguousarray(xg, dtype=np.float64)
     gw = np.ascontiguousarray(wg, dtype=np.float64)
     out = C.c_double(0.0)
-    L.check(L.lib().hw_l2err2d(C.byref(rows2d(f)), int(mx), int(my), C.byref(g), float(grid.x_left),
+    r = rows if rows is not None else rows2d(f)
+    L.check(L.lib().hw_l2err2d(C.byref(r), int(mx), int(my), C.byref(g), float(grid.x_left),
                                float(grid.y_left), grid.hx, grid.hy, int(npts), gx.ctypes.data_as(C.c_void_p),
                                gw.ctypes.data_as(C.c_void_p), int(kind),
                                ptr(ex_dev) if ex_dev is not None else None, params, C.byref(out), st.stream),
             "l2_error_field_2d")
-    return math.sqrt(out.value)
+    return out.value
+
+
+def l2_error_field_2d(field: Field2D, exact, bc: BoundarySpec2D, npts: int | None = None) -> float:
+    """L2 error of the global tensor interpolant (diagnostics.py:118-135).
+
+    Like the reference, cells are the targets of the field's own corner
+    gather (no clipping in 2D)."""
+    mx, my = field.orders
+    npts = npts or default_npts(max(mx, my))
+    st = Staging(field.values)
+    f = st.to_dev(field.values)
+    return math.sqrt(_l2_sum_2d(f, field.grid, field.parity, (mx, my), exact, bc, npts))
 
 
 def _pieces_1d(field: Field1D):

@@ -4,9 +4,12 @@ size-independent properties (the oracle cannot step a whole 16384^2 grid):
   * C2 (periodic m=4, 1024^2) and C5 at its single-GPU size (m=6, 8192^2): one device half step,
     then oracle windows (rows x columns, periodic wrap) at the grid's
     corners and middle;
-  * C3 (conservative m=5, 2048^2, Dirichlet x / Neumann y): time reversal —
-    N steps forward, swap the levels, N steps back returns the start (the
-    two-level update is exactly reversible, SURVEY App. A.7);
+  * C3 (conservative m=5, 2048^2, Dirichlet x / Neumann y): reversibility —
+    N steps forward, swap the levels, N steps back returns the start.  Any
+    update new = F(cur) - prev has this property, so it checks the in-place
+    two-level bookkeeping, not the operator: the operator at full size is
+    pinned by tests/test_c3.py's wall-corner oracle windows and the energy by
+    tests/test_energy_cons2d.py;
   * 2D -> 1D reduction on y-independent data (test_dissipative.py:266-302,
     test_conservative.py:212-238).
 """
