@@ -242,6 +242,23 @@ int hw_init_planewave2d(double* out, int64_t nx, int64_t ny, int64_t row0, int k
                         double kappa, double hx, double hy, int tder,
                         void* stream);
 
+/* driver.py:195-200 _scale_cols: out[r][l] = in[r][l] * h^l / l! (may alias). */
+int hw_scale_cols(const double* in, double* out, int64_t rows, int cols, double h, void* stream);
+
+/*
+ * driver.py:195-238 closed-form 1D initial data on the device: out[i][k],
+ * k = 0..kmax, the k-th x-derivative of
+ *   kind 0: exp(a x^2)                    (gaussian_derivs)
+ *   kind 1: (G(x+t) + G(x-t))/2, G = exp(a x^2); tder = 1 its time
+ *           derivative (G'(x+t) - G'(x-t))/2   (gaussian_box_u / _v)
+ *   kind 2: sin(x) cos(t)                 (sine_derivs)
+ * at x[i] (device array) or, with x = NULL, at x0 + h*(i+off); scaled != 0
+ * multiplies column k by h^k/k! (_scale_cols, driver.py:195-200).
+ */
+int hw_init_1d(double* out, const double* x, int64_t n, int kmax, int kind,
+               double x0, double h, double off, int scaled, double t, double a,
+               int tder, void* stream);
+
 /*
  * Standing wave u = sin(ax x) sin(ay y) cos(om t) (tder = 0) or u_t
  * (tder = 1) as scaled blocks; with trig shift phases (px, py) so that

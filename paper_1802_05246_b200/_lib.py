@@ -26,7 +26,7 @@ EXPORTS = (
     "hw_diss2d_half_step", "hw_cons2d_step", "hw_boot2d", "hw_diss1d_half_step",
     "hw_cons1d_step", "hw_boot1d", "hw_l2err2d", "hw_l2err1d", "hw_count_nonfinite",
     "hw_init_planewave2d", "hw_init_standing2d", "hw_cell_map_dims", "hw_cell_map_2d",
-    "hw_seminorm1d", "hw_cons_energy1d", "hw_seminorm2d", "hw_inner2d",
+    "hw_seminorm1d", "hw_cons_energy1d", "hw_seminorm2d", "hw_inner2d", "hw_init_1d", "hw_scale_cols",
     "hw_apply_interp", "hw_apply_interp_2d", "hw_expand_taylor", "hw_expand_taylor_2d", "hw_eval_series",
     "hw_cons_update_1d", "hw_cons_update_2d", "hw_gather", "hw_ghost",
 )
@@ -100,6 +100,8 @@ def _declare(lib):
                                C.POINTER(_D), _P]),
         "hw_inner2d": (_I, [C.POINTER(Rows2D), C.POINTER(Rows2D), _I, _I, C.POINTER(Geom2D), _D, _D, _I, _I, _I,
                             _P, _P, _I, C.POINTER(_D), _P]),
+        "hw_scale_cols": (_I, [_P, _P, _L, _I, _D, _P]),
+        "hw_init_1d": (_I, [_P, _P, _L, _I, _I, _D, _D, _D, _I, _D, _D, _I, _P]),
         "hw_init_planewave2d": (_I, [_P, _L, _L, _L, _I, _I, _D, _D, _D, _D, _D, _D, _D, _I, _P]),
         "hw_init_standing2d": (_I, [_P, _L, _L, _L, _I, _I, _D, _D, _D, _D, _D, _D, _D, _D, _D,
                                     _D, _D, _I, _P]),

@@ -959,6 +959,16 @@ int hw_ghost(const double* in, double* out, int64_t batch, int n0, int n1, int a
   });
 }
 
+int hw_scale_cols(const double* in, double* out, int64_t rows, int cols, double h, void* stream) {
+  return guard([&] {
+    HW_CHECK(rows >= 0 && cols >= 1, "sizes out of range");
+    if (rows == 0) return;
+    HW_CHECK(in && out, "null pointer");
+    scale_cols_kernel<<<ll_blocks(rows * cols), 128, 0, (cudaStream_t)stream>>>(in, out, rows, cols, h);
+    cuda_check(cudaGetLastError(), "scale_cols launch");
+  });
+}
+
 int hw_count_nonfinite(const double* x, int64_t n, int64_t* out_host, void* stream) {
   return guard([&] {
     HW_CHECK(out_host, "null output");
@@ -1046,6 +1056,34 @@ int hw_init_standing2d(double* out, int64_t nx, int64_t ny, int64_t row0, int kx
     a.om = om;
     a.tder = tder;
     launch_init(a, (cudaStream_t)stream);
+  });
+}
+
+int hw_init_1d(double* out, const double* x, int64_t n, int kmax, int kind, double x0, double h, double off,
+               int scaled, double t, double a, int tder, void* stream) {
+  return guard([&] {
+    HW_CHECK(out, "null output");
+    HW_CHECK(n >= 0, "node count must be nonnegative");
+    HW_CHECK(kmax >= 0 && kmax <= kMax1D, "derivative count out of range (0..12)");
+    HW_CHECK(kind >= 0 && kind <= 2, "unknown 1D data kind");
+    HW_CHECK(tder == 0 || (tder == 1 && kind == 1), "only the gaussian box has a time derivative");
+    if (n == 0) return;
+    Init1DArgs g;
+    std::memset(&g, 0, sizeof(g));
+    g.out = out;
+    g.xs = x;
+    g.n = n;
+    g.kmax = kmax;
+    g.kind = kind;
+    g.tder = tder;
+    g.scaled = scaled != 0;
+    g.x0 = x0;
+    g.h = h;
+    g.off = off;
+    g.t = t;
+    g.a = a;
+    init1d_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(g);
+    cuda_check(cudaGetLastError(), "init1d launch");
   });
 }
 

@@ -331,6 +331,53 @@ struct Init2DArgs {
   int tder;
 };
 
+// driver.py:195-238 closed-form 1D initial data, one thread per node:
+// derivative columns d^k/dx^k (k = 0..kmax) of
+//   kind 0  G(x) = exp(a x^2)                          (gaussian_derivs)
+//   kind 1  (G(x+t) + G(x-t)) / 2, tder 1: its u_t     (gaussian_box_u / _v)
+//   kind 2  sin(x) cos(t)                              (sine_derivs)
+// optionally scaled by h^k / k! (_scale_cols).  Gaussian derivatives by the
+// Leibniz recurrence G^(k+1) = 2a (x G^(k) + k G^(k-1)) (G' = 2 a x G).
+struct Init1DArgs {
+  double* out;
+  const double* xs;  // node coordinates (NULL: x = x0 + h (i + off))
+  int64_t n;
+  int kmax, kind, tder, scaled;
+  double x0, h, off, t, a;
+};
+
+__device__ inline void gauss_cols(double x, double a, int kmax, double* d) {
+  const double g = exp(a * x * x);
+  d[0] = g;
+  if (kmax >= 1) d[1] = 2.0 * a * x * g;
+  for (int k = 1; k < kmax; ++k) d[k + 1] = 2.0 * a * (x * d[k] + (double)k * d[k - 1]);
+}
+
+__global__ void init1d_kernel(Init1DArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  const double x = a.xs ? a.xs[i] : a.x0 + a.h * ((double)i + a.off);
+  double col[kMax1D + 3];
+  if (a.kind == 0) {
+    gauss_cols(x, a.a, a.kmax, col);
+  } else if (a.kind == 1) {
+    double gp[kMax1D + 3], gm[kMax1D + 3];
+    gauss_cols(x + a.t, a.a, a.kmax + 1, gp);
+    gauss_cols(x - a.t, a.a, a.kmax + 1, gm);
+    // u = (G(x+t) + G(x-t)) / 2, u_t = (G'(x+t) - G'(x-t)) / 2
+    for (int k = 0; k <= a.kmax; ++k)
+      col[k] = a.tder ? 0.5 * (gp[k + 1] - gm[k + 1]) : 0.5 * (gp[k] + gm[k]);
+  } else {
+    const double ct = cos(a.t);
+    for (int k = 0; k <= a.kmax; ++k) col[k] = sin(x + 0.5 * 3.141592653589793 * (double)k) * ct;
+  }
+  double fac = 1.0;
+  for (int k = 0; k <= a.kmax; ++k) {
+    if (k > 0 && a.scaled) fac = fac * a.h / (double)k;  // driver.py:195-200 running factor
+    a.out[i * (a.kmax + 1) + k] = a.scaled ? col[k] * fac : col[k];
+  }
+}
+
 __global__ void init2d_kernel(Init2DArgs a) {
   const int64_t node = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (node >= a.nx * a.ny) return;
@@ -354,9 +401,6 @@ __global__ void init2d_kernel(Init2DArgs a) {
       }
     }
   } else {
-    const double sxv = 0, syv = 0;
-    (void)sxv;
-    (void)syv;
     for (int k = 0; k < wx; ++k) {
       double fk = 1.0;
       for (int q = 2; q <= k; ++q) fk *= q;

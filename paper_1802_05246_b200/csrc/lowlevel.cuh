@@ -215,4 +215,15 @@ __global__ void ghost_kernel(const double* in, double* out, int64_t batch, int n
   out[idx] = v;
 }
 
+// driver.py:195-200 _scale_cols: column l of every row times h^l / l!, the
+// factor built by the same running product fac[l] = fac[l-1] * h / l.
+__global__ void scale_cols_kernel(const double* in, double* out, int64_t rows, int cols, double h) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= rows * cols) return;
+  const int l = (int)(idx % cols);
+  double fac = 1.0;
+  for (int q = 1; q <= l; ++q) fac = fac * h / (double)q;
+  out[idx] = in[idx] * fac;
+}
+
 }  // namespace hw
