@@ -18,7 +18,7 @@ def _run(n):
     import torch
 
     import paper_1802_05246_b200 as hb
-    from paper_1802_05246_b200.studies import scale_cols, sine_derivs
+    from oracle.hermite_oracle import scale_cols, sine_derivs  # the reference's own input bits
 
     grid = hb.Grid1D(0.0, 2.0 * math.pi, n, True)
     h = grid.h
@@ -66,7 +66,7 @@ def test_c1_nx200_final_state_matches_reference():
     # the reference algorithm's own sensitivity (oracle, 1-ulp input
     # perturbation, same 71 half steps: SURVEY App. A.4)
     from oracle import hermite_oracle as O
-    from paper_1802_05246_b200.studies import scale_cols, sine_derivs
+    from oracle.hermite_oracle import scale_cols, sine_derivs
 
     n, h = 200, 2.0 * math.pi / 200
     u0 = scale_cols(sine_derivs(O.nodes(0.0, h, n, True, O.PRIMAL), M, 0.0), h)
