@@ -84,6 +84,10 @@ def _as_device_nodes(x):
 def _columns(x, kmax: int, kind: str, t: float = 0.0, a: float = -20.0, tder: int = 0):
     xd, host, shp = _as_device_nodes(x)
     out = require_cuda().empty(shp + (int(kmax) + 1,), dtype=xd.dtype, device=xd.device)
+    if xd.numel() == 0:
+        if not 0 <= kmax <= 12:
+            raise ValueError(f"{kind}: derivative count out of range (0..12)")
+        return out.cpu().numpy() if host else out
     L.check(L.lib().hw_init_1d(out.data_ptr(), xd.data_ptr(), int(xd.numel()), int(kmax), _KIND_1D[kind], 0.0,
                                0.0, 0.0, 0, float(t), float(a), int(tder), stream_handle(xd.device)), kind)
     return out.cpu().numpy() if host else out

@@ -90,7 +90,9 @@ def test_criteria_1_to_3_rates_match_reference(acc_gold, exp, scheme, m, lam):
     rep = S.run_experiment(cfg)
     k = f"{exp}/{scheme[:4]}/m{m}/lam{lam}"
     np.testing.assert_array_equal(rep.ns, acc_gold[f"{k}/ns"])
-    np.testing.assert_allclose(rep.err_u, acc_gold[f"{k}/err_u"], rtol=1e-9, atol=1e-15)
+    # initial data come from the device generators (ulp-level differences from the reference's numpy
+    # evaluation, tests/test_init1d.py), so errors near round-off carry an absolute floor
+    np.testing.assert_allclose(rep.err_u, acc_gold[f"{k}/err_u"], rtol=1e-9, atol=1e-14)
     assert rep.rate() == pytest.approx(float(acc_gold[f"{k}/rate"]), abs=1e-6)
 
 

@@ -5,7 +5,8 @@ tests/golden/make_golden_init1d.py from hermwave.driver:195-238).
 The device evaluates the Gaussian derivatives by the Leibniz recurrence
 G^(k+1) = 2a (x G^(k) + k G^(k-1)) instead of the reference's polynomial
 coefficients + polyval, so the two agree to rounding: per derivative column,
-relative to the column's largest magnitude.
+relative to the column's largest magnitude (sin(x + k pi/2) is CUDA's sin of a
+shifted argument vs numpy's: a few ulp of the column max).
 """
 
 import math
@@ -56,7 +57,7 @@ def test_device_generators_at_points(g1, k):
     _cols_close(hb.gaussian_derivs(x, k, a=-3.0), g1[f"pts/gauss_a3/{k}"])
     _cols_close(hb.gaussian_box_u(x, 0.37, k), g1[f"pts/box_u/{k}"])
     _cols_close(hb.gaussian_box_v(x, 0.37, k), g1[f"pts/box_v/{k}"])
-    _cols_close(hb.sine_derivs(x, k, 0.8), g1[f"pts/sine/{k}"], 1e-15)
+    _cols_close(hb.sine_derivs(x, k, 0.8), g1[f"pts/sine/{k}"], 1e-14)
 
 
 @pytest.mark.gpu
@@ -78,7 +79,7 @@ def test_device_scaled_data_on_grids(g1, m, n, lam):
         _cols_close(data_on_grid_1d(g, par, "gaussian_box", m, t=0.0, tder=1, host=True),
                     g1[f"grid/{m}/{n}/{par}/box_v"])
         _cols_close(data_on_grid_1d(gp, par, "sine", m, t=-0.5 * lam * gp.h, host=True),
-                    g1[f"grid/{m}/{n}/{par}/sine"], 1e-15)
+                    g1[f"grid/{m}/{n}/{par}/sine"], 1e-14)
         # scale_cols on the device == the reference's _scale_cols of the same columns
         x = g.nodes(par)
         raw = hb.gaussian_derivs(torch.as_tensor(x, device="cuda"), m)
