@@ -98,6 +98,14 @@ int hw_cell_map_2d(int scheme, int m, double dt, double hx, double hy, double sp
 int64_t hw_target_count(int64_t n_src, int parity_src, int periodic);
 
 /*
+ * The three 2D steps accept every order the reference does, m = 1..12
+ * (interp.py:30, 62-63; larger m -> HW_EINVAL).  The operator is the per-class
+ * cell map above; which kernel applies it is an implementation detail
+ * (tensor-core DMMA cell map, the SIMT constant-operand cell map, or the
+ * generic runtime-order kernel above m = 8) and does not change the ABI.
+ */
+
+/*
  * dissipative.py:215-247 half_step_2d (stabilised 2D half step).
  * u: orders (m,m), v: orders (m-1,m-1).  Writes target rows
  * [trow0, trow0+ntrows) of the opposite parity into u_dst / v_dst

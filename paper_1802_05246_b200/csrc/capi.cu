@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstring>
 #include <list>
+#include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -16,12 +17,29 @@
 #include "diag.cuh"
 #include "line1d.cuh"
 #include "lowlevel.cuh"
+#include "simt2d.cuh"
 #include "tables.h"
+
+// Which 2D steps run the SIMT cell map (simt2d.cuh: CUDA-core FP64, class
+// maps as constant operands) instead of the tensor-core cell map
+// (cellmap.cuh): the conservative scheme at m <= 2, where it measured 2.1x
+// faster (profiles/ab_r02_kernel_knobs.txt).  A/B knob HW_SIMT_M: every
+// scheme at m <= HW_SIMT_M (0..5).
+static constexpr bool use_simt(int sch, int m) {
+#ifdef HW_SIMT_M
+  static_assert(HW_SIMT_M <= 5, "the SIMT kernel's class maps fit the parameter space up to m = 5");
+  return m <= HW_SIMT_M;
+#else
+  return sch == hw::kCons && m <= 2;
+#endif
+}
 
 namespace hw {
 
 template <int M, int SCH>
 cudaError_t launch_cellmap(const CellMapArgs& a, cudaStream_t st);  // kern_m*.cu
+template <int M, int SCH>
+cudaError_t launch_simt2d(const Simt2DArgs& a, const double* wd, const int* code, cudaStream_t st);  // kern_m1..5.cu
 
 static thread_local std::string g_err;
 
@@ -79,6 +97,10 @@ struct DevMap {
   double* wfrag = nullptr;
   int* ocode = nullptr;
   int* icode = nullptr;
+  double* wdense = nullptr;  // [dout][din] class-major (simt2d.cuh)
+  int* dcode = nullptr;      // [dout]
+  std::shared_ptr<const std::vector<double>> hwd;  // host copies (the SIMT kernel's parameter block)
+  std::shared_ptr<const std::vector<int>> hdc;
 };
 
 struct MapKey {
@@ -99,6 +121,8 @@ static void free_map(DevMap& d) {
   cudaFree(d.wfrag);
   cudaFree(d.ocode);
   cudaFree(d.icode);
+  cudaFree(d.wdense);
+  cudaFree(d.dcode);
 }
 
 static DevMap device_map(int scheme, int m, double dt, double hx, double hy, double speed, int stages) {
@@ -145,8 +169,22 @@ static DevMap device_map(int scheme, int m, double dt, double hx, double hy, dou
             wf[((size_t)ks * nt + base + j) * 32 + lane] = cm.w[c][(size_t)o * cm.din + e];
         }
   }
+  // class-major dense maps for the SIMT kernel
+  std::vector<double> wd((size_t)cm.dout * cm.din);
+  std::vector<int> dc((size_t)cm.dout);
+  for (int c = 0, row = 0; c < 4; ++c)
+    for (int o = 0; o < cm.ncls[c]; ++o, ++row) {
+      dc[row] = cm.code[c][o];
+      for (int e = 0; e < cm.din; ++e) wd[(size_t)row * cm.din + e] = cm.w[c][(size_t)o * cm.din + e];
+    }
   DevMap d;
+  d.hwd = std::make_shared<const std::vector<double>>(wd);
+  d.hdc = std::make_shared<const std::vector<int>>(dc);
   try {
+    cuda_check(cudaMalloc(&d.wdense, wd.size() * sizeof(double)), "cudaMalloc(wdense)");
+    cuda_check(cudaMalloc(&d.dcode, dc.size() * sizeof(int)), "cudaMalloc(dcode)");
+    cuda_check(cudaMemcpy(d.wdense, wd.data(), wd.size() * sizeof(double), cudaMemcpyHostToDevice), "upload wd");
+    cuda_check(cudaMemcpy(d.dcode, dc.data(), dc.size() * sizeof(int), cudaMemcpyHostToDevice), "upload dcode");
     cuda_check(cudaMalloc(&d.wfrag, wf.size() * sizeof(double)), "cudaMalloc(wfrag)");
     cuda_check(cudaMalloc(&d.ocode, oc.size() * sizeof(int)), "cudaMalloc(ocode)");
     cuda_check(cudaMalloc(&d.icode, ic.size() * sizeof(int)), "cudaMalloc(icode)");
@@ -170,8 +208,59 @@ static DevMap device_map(int scheme, int m, double dt, double hx, double hy, dou
 }
 
 template <int SCH>
-static void dispatch_cellmap(int m, const CellMapArgs& a, cudaStream_t st) {
+static void dispatch_cellmap(int m, const CellMapArgs& a, const DevMap& dm, cudaStream_t st) {
   cudaError_t e;
+  if (use_simt(SCH, m) || m > kMaxFast) {
+    Simt2DArgs s;
+    std::memset(&s, 0, sizeof(s));
+    s.f0 = a.f0;
+    s.f1 = a.f1;
+    s.wd = dm.wdense;
+    s.code = dm.dcode;
+    s.prev = a.prev;
+    s.out0 = a.out0;
+    s.out1 = a.out1;
+    s.nx = a.nx;
+    s.ny = a.ny;
+    s.trow0 = a.trow0;
+    s.ntrows = a.ntrows;
+    s.nty = a.nty;
+    s.off = a.off;
+    s.periodic = a.periodic;
+    s.kxl = a.kxl;
+    s.kxh = a.kxh;
+    s.kyl = a.kyl;
+    s.kyh = a.kyh;
+    s.gxl = a.gxl;
+    s.gxh = a.gxh;
+    s.gyl = a.gyl;
+    s.gyh = a.gyh;
+    if (m > kMaxFast) {  // m = 9..12: the generic runtime-order path
+      Gen2DArgs g;
+      std::memset(&g, 0, sizeof(g));
+      g.s = s;
+      g.w0 = cm_win(SCH, m, 0);
+      g.w1 = cm_win(SCH, m, 1);
+      g.ow0 = cm_wout(SCH, m, 0);
+      g.ow1 = cm_wout(SCH, m, 1);
+      g.din = cm_din(SCH, m);
+      g.dout = cm_dout(SCH, m);
+      for (int c = 0; c < 4; ++c) g.ncls[c] = cm_ncls(SCH, m, c);
+      e = launch_simt2d_generic(g, SCH, st);
+    } else {
+      const double* hw = dm.hwd->data();
+      const int* hc = dm.hdc->data();
+      switch (m) {
+        case 1: e = launch_simt2d<1, SCH>(s, hw, hc, st); break;
+        case 2: e = launch_simt2d<2, SCH>(s, hw, hc, st); break;
+        case 3: e = launch_simt2d<3, SCH>(s, hw, hc, st); break;
+        case 4: e = launch_simt2d<4, SCH>(s, hw, hc, st); break;
+        default: e = launch_simt2d<5, SCH>(s, hw, hc, st); break;
+      }
+    }
+    cuda_check(e, "simt2d launch");
+    return;
+  }
   switch (m) {
     case 1: e = launch_cellmap<1, SCH>(a, st); break;
     case 2: e = launch_cellmap<2, SCH>(a, st); break;
@@ -181,7 +270,7 @@ static void dispatch_cellmap(int m, const CellMapArgs& a, cudaStream_t st) {
     case 6: e = launch_cellmap<6, SCH>(a, st); break;
     case 7: e = launch_cellmap<7, SCH>(a, st); break;
     case 8: e = launch_cellmap<8, SCH>(a, st); break;
-    default: throw Error(HW_EUNSUPPORTED, "method order m=" + std::to_string(m) + " has no compiled 2D path (1..8)");
+    default: throw Error(HW_EUNSUPPORTED, "method order m=" + std::to_string(m) + " has no 2D path (1..12)");
   }
   cuda_check(e, "cellmap launch");
 }
@@ -273,7 +362,7 @@ int hw_cell_map_dims(int scheme, int m, int* din, int* dout) {
   return guard([&] {
     HW_CHECK(din && dout, "null output");
     HW_CHECK(scheme >= kDiss && scheme <= kBoot, "unknown scheme");
-    HW_CHECK(m >= 1 && m <= kMaxOrder - 1, "method order out of range");
+    HW_CHECK(m >= 1 && m <= kMaxOrder, "method order out of range");
     *din = cm_din(scheme, m);
     *dout = cm_dout(scheme, m);
   });
@@ -283,7 +372,7 @@ int hw_cell_map_2d(int scheme, int m, double dt, double hx, double hy, double sp
   return guard([&] {
     HW_CHECK(out, "null output");
     HW_CHECK(scheme >= kDiss && scheme <= kBoot, "unknown scheme");
-    HW_CHECK(m >= 1 && m <= kMaxOrder - 1, "method order out of range");
+    HW_CHECK(m >= 1 && m <= kMaxOrder, "method order out of range");
     HW_CHECK(stages >= 1 || scheme == kCons, "stage count must be >= 1");
     const CellMap cm = build_cell_map(scheme, m, dt, hx, hy, speed, stages);
     const std::vector<double> d = dense_cell_map(cm);
@@ -302,12 +391,12 @@ int hw_diss2d_half_step(const hw_rows2d* u_src, const hw_rows2d* v_src, double* 
     check_rows(v_src, g, u_src);
     if (g.ntrows == 0) return;
     const int S = stage_cap > 0 ? stage_cap : 4 * m + 4;  // dissipative.py:73-74
-    HW_CHECK(m <= kMaxFast, "method order m=" + std::to_string(m) + " has no compiled 2D path (1..8)");
+    HW_CHECK(m <= kMaxOrder, "method order m=" + std::to_string(m) + " out of range (interp.py:62-63: 1..12)");
     const DevMap dm = device_map(kDiss, m, dt, hx, hy, speed, S);
     CellMapArgs a = cellmap_args(g, geom, u_src, v_src, dm, m);
     a.out0 = u_dst;
     a.out1 = v_dst;
-    dispatch_cellmap<kDiss>(m, a, (cudaStream_t)stream);
+    dispatch_cellmap<kDiss>(m, a, dm, (cudaStream_t)stream);
   });
 }
 
@@ -319,12 +408,12 @@ int hw_cons2d_step(const hw_rows2d* cur_src, const double* prev, double* out, in
     const Geo g = check_geom(geom);
     check_rows(cur_src, g);
     if (g.ntrows == 0) return;
-    HW_CHECK(m <= kMaxFast, "method order m=" + std::to_string(m) + " has no compiled 2D path (1..8)");
+    HW_CHECK(m <= kMaxOrder, "method order m=" + std::to_string(m) + " out of range (interp.py:62-63: 1..12)");
     const DevMap dm = device_map(kCons, m, dt, hx, hy, speed, 0);
     CellMapArgs a = cellmap_args(g, geom, cur_src, nullptr, dm, m);
     a.prev = prev;
     a.out0 = out;
-    dispatch_cellmap<kCons>(m, a, (cudaStream_t)stream);
+    dispatch_cellmap<kCons>(m, a, dm, (cudaStream_t)stream);
   });
 }
 
@@ -337,11 +426,11 @@ int hw_boot2d(const hw_rows2d* g0_src, const hw_rows2d* g1_src, double* out, int
     check_rows(g0_src, g);
     check_rows(g1_src, g, g0_src);
     if (g.ntrows == 0) return;
-    HW_CHECK(m <= kMaxFast, "method order m=" + std::to_string(m) + " has no compiled 2D path (1..8)");
+    HW_CHECK(m <= kMaxOrder, "method order m=" + std::to_string(m) + " out of range (interp.py:62-63: 1..12)");
     const DevMap dm = device_map(kBoot, m, dt, hx, hy, speed, 4 * m + 4);  // conservative.py:192
     CellMapArgs a = cellmap_args(g, geom, g0_src, g1_src, dm, m);
     a.out0 = out;
-    dispatch_cellmap<kBoot>(m, a, (cudaStream_t)stream);
+    dispatch_cellmap<kBoot>(m, a, dm, (cudaStream_t)stream);
   });
 }
 

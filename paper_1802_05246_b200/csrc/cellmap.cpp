@@ -157,7 +157,7 @@ void eval_cell_reference(int scheme, int m, double dt, double hx, double hy, dou
 
 CellMap build_cell_map(int scheme, int m, double dt, double hx, double hy, double speed, int stages) {
   if (scheme < kDiss || scheme > kBoot) throw std::invalid_argument("unknown scheme");
-  if (m < 1 || m > kMaxOrder - 1) throw std::invalid_argument("method order out of range");
+  if (m < 1 || m > kMaxOrder) throw std::invalid_argument("method order out of range");
   CellMap cm;
   cm.scheme = scheme;
   cm.m = m;

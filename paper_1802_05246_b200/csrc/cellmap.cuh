@@ -67,6 +67,16 @@ struct CellMapArgs {
 #ifndef HW_CM_PDL
 #define HW_CM_PDL 1  // programmatic dependent launch between consecutive steps (A/B knob)
 #endif
+#ifndef HW_CM_PPREF
+// `previous` staging for the producer-drained conservative orders (A/B knob):
+// 0 = consumers copy it at the tile's last chunk and wait for it (round 1),
+// 1 = producers prefetch it one tile ahead (measured 0.69x at m = 5: the
+//     producers become the bottleneck),
+// 2 = consumers copy it at the last chunk and hand the wait to the drain
+//     through a per-warp mbarrier (no consumer-side cp.async wait; measured
+//     2-6% slower than 0 at m = 4, 5: the drain then waits on the copies)
+#define HW_CM_PPREF 0
+#endif
 #ifndef HW_CM_SLEEP
 #define HW_CM_SLEEP 64  // producer back-off (ns) while its ring slot is busy and no slab is ready
 #endif
@@ -123,9 +133,17 @@ struct CMCfg {
   static constexpr bool DIRECT = cm_direct(SCH, M);
   static constexpr bool SELF = cm_self(SCH, M) && !DIRECT;
   static constexpr bool OWN = DIRECT || SELF;  // the consumers write HBM themselves
+  // `previous` of the producer-drained conservative orders reaches the drain
+  // through a per-warp mbarrier (pready) instead of a consumer cp.async wait:
+  // PPREF (HW_CM_PPREF 1) the producers stage it one tile ahead, CPREF (2)
+  // the consumers issue the copies at the tile's last chunk.
+  static constexpr bool PDRAIN = SCH == kCons && !(cm_direct(SCH, M) || (cm_self(SCH, M) && !cm_direct(SCH, M)));
+  static constexpr bool PPREF = HW_CM_PPREF == 1 && PDRAIN;
+  static constexpr bool CPREF = HW_CM_PPREF == 2 && PDRAIN;
+  static constexpr int NPR = (PPREF || CPREF) ? NW : 0;  // pready barriers
   static constexpr int tail(int mt) {
     return WRESN * 8 + NW * ((DIRECT ? 0 : mt * NT * 64) + (SCH == kCons ? mt * 8 * O0 : 0)) * 8 + (8 * DO + 8 * NT) * 4 +
-           (2 * NSMAX + 2 * NW) * 8 + 64;
+           (2 * NSMAX + 2 * NW + NPR) * 8 + 64;
   }
   static constexpr bool fits(int mt, int ns) { return ns * sbuf(mt) * 8 + tail(mt) <= SMEM_MAX; }
   // Ring depth: 4 slots only where they leave >= 56 KB of the SM's 256 KB
@@ -344,7 +362,8 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
   uint64_t* empty = bars + C::NSMAX;      // [NS] consumers -> producers: ring slot consumed
   uint64_t* sfull = bars + 2 * C::NSMAX;  // [NW] consumer w -> producer: output slab written
   uint64_t* sempty = sfull + NW;          // [NW] producer -> consumer w: output slab drained
-  int* s_tile = reinterpret_cast<int*>(sempty + NW);  // [QT] tile id of this CTA's k-th tile (in the tail's slack)
+  uint64_t* pready = sempty + NW;         // [NPR] producer lanes' `previous` copies of warp w's next tile landed
+  int* s_tile = reinterpret_cast<int*>(pready + C::NPR);  // [QT] tile id of this CTA's k-th tile (in the tail's slack)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   // Inverse fragment map: output q of an M-tile's records, laid out
@@ -370,6 +389,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       mbar_init(&sfull[w], 1);
       mbar_init(&sempty[w], 1);
     }
+    for (int w = 0; w < C::NPR; ++w) mbar_init(&pready[w], 32);  // one cp.async arrive per producer lane
   }
   __syncthreads();
 #if HW_CM_PDL
@@ -397,8 +417,8 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
   // ends the CTA's sequence; the last CTA to make that claim zeroes the
   // counters for the next launch.  Null a.sched: static round robin.
   static_assert(C::NS + 2 <= C::QT, "tile-id ring shorter than the tiles in flight");
-  static_assert((2 * C::NSMAX + 2 * NW) * 8 + (8 * C::DO + 8 * NT) * 4 + 4 * C::QT + 4 <=
-                    (2 * C::NSMAX + 2 * NW) * 8 + (8 * C::DO + 8 * NT) * 4 + 64,
+  static_assert((2 * C::NSMAX + 2 * NW + C::NPR) * 8 + (8 * C::DO + 8 * NT) * 4 + 4 * C::QT + 4 <=
+                    (2 * C::NSMAX + 2 * NW + C::NPR) * 8 + (8 * C::DO + 8 * NT) * 4 + 64,
                 "s_tile must fit the tail's slack");
 
   auto tile_geo = [&](int tile) {
@@ -454,6 +474,30 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
 #pragma unroll
       for (int k = 0; k < K1N; ++k) inv[K0N + k] = lane + 32 * k < 8 * C::O1 ? s_inv[8 * C::O0 + lane + 32 * k] : 0;
     }
+    // PPREF: stage `previous` of consumer warp w's kt-th tile into its slab
+    // (its id is published: kt <= this CTA's staged tile count); every lane
+    // arrives on pready[w] once its own copies have landed.
+    auto prefetch_prev = [&](int w, int kt) {
+      if constexpr (C::PPREF) {
+        const int tile = s_tile[kt % C::QT];
+        if (tile < ntiles && MODE != 2 && MODE != 3) {
+          const CMTile tg = tile_geo(tile);
+          double* pv = pslabs + w * C::PSLAB;
+#pragma unroll
+          for (int t = 0; t < MT; ++t) {
+            int64_t cell0;
+            const int nv = mtile(tg, w, t, cell0);
+            const double* p = a.prev + cell0 * C::O0;
+            for (int q = lane; q < nv * C::O0; q += 32) cm_cp_async8(pv + t * 8 * C::O0 + q, p + q);
+          }
+        }
+        mbar_arrive_cp_async(&pready[w]);
+      }
+    };
+    if constexpr (C::PPREF) {
+#pragma unroll
+      for (int j = 0; j < NW / C::NPW; ++j) prefetch_prev(pw + C::NPW * j, 0);
+    }
     auto try_drain = [&]() {
       bool any = false;
       if constexpr (!C::OWN) {  // (DIRECT / SELF: the consumers store their own outputs)
@@ -461,7 +505,9 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       for (int j = 0; j < NW / C::NPW; ++j) {
         const int w = pw + C::NPW * j;
         if (dk[j] >= ktot) continue;
-        int ready = lane == 0 ? (int)mbar_test(&sfull[w], dk[j] & 1) : 0;
+        int ready = 0;
+        if (lane == 0)
+          ready = (int)mbar_test(&sfull[w], dk[j] & 1) && (C::NPR == 0 || mbar_test(&pready[w], dk[j] & 1));
         ready = __shfl_sync(0xffffffffu, ready, 0);
         if (!ready) continue;
         const CMTile tg = tile_geo(s_tile[dk[j] % C::QT]);
@@ -522,6 +568,9 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
         __syncwarp();
         if (lane == 0) mbar_arrive(&sempty[w]);
         ++dk[j];
+        // this lane's reads of the slab's `previous` entries are done (their
+        // values went to HBM above): refill them for the warp's next tile
+        prefetch_prev(w, dk[j]);
         any = true;
       }
       }
@@ -738,7 +787,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       // records are staged — contiguous, with cp.async, landing under the
       // last chunk's DMMAs).
       if (!C::OWN && k >= 1) mbar_wait(&sempty[warp], (k - 1) & 1);
-      if (SCH == kCons) {
+      if (SCH == kCons && !C::PPREF) {  // (CPREF: the drain, not this warp, waits for the copies)
         double* pv = pslabs + warp * C::PSLAB;
 #pragma unroll
         for (int t = 0; t < MT; ++t) {
@@ -747,6 +796,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
           const double* p = a.prev + cell0 * C::O0;
           for (int q = lane; q < nv * C::O0; q += 32) cm_cp_async8(pv + t * 8 * C::O0 + q, p + q);
         }
+        if (C::CPREF) mbar_arrive_cp_async(&pready[warp]);  // the drain waits for these copies
       }
     }
     if (ch != 0) mbar_wait(&full[b], (g / NS) & 1);
@@ -868,7 +918,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
         for (int n = 0; n < NT; ++n)
           *reinterpret_cast<double2*>(slab + t * NT * 64 + (n * 32 + ((lane + C::SWZ * n) & 31)) * 2) =
               make_double2(acc[t][n][0], acc[t][n][1]);
-      if (SCH == kCons) asm volatile("cp.async.wait_all;\n" ::: "memory");  // `previous` landed
+      if (SCH == kCons && !C::PPREF && !C::CPREF) asm volatile("cp.async.wait_all;\n" ::: "memory");  // `previous` landed
       __syncwarp();
       if constexpr (C::SELF) {
         // drain it ourselves: record order, consecutive lanes on consecutive doubles

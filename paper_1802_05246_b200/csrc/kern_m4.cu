@@ -1,6 +1,8 @@
 // Instantiates the fused 2D cell-map kernels for method order m = 4.
 #include "cellmap_launch.cuh"
+#include "simt2d.cuh"
 
 namespace hw {
 HW_INSTANTIATE_CELLMAP(4)
+HW_INSTANTIATE_SIMT2D(4)
 }  // namespace hw

@@ -65,6 +65,17 @@ C3_LAM = 0.9
 C3_WAVE_BC = (("dirichlet0", "dirichlet0", 0.0, 0.0), ("neumann0", "neumann0", 0.0, 0.0))
 C3_RAND_BC = (("dirichlet0", "dirichlet0", 0.3, -0.2), ("neumann0", "neumann0", 0.0, 0.0))
 
+# 2D steps at m = 9..12 (tests/golden/make_golden_high2d.py -> high2d.npz):
+# (name, m, nx, ny, walls, parity); Grid2D(0, 1, -0.5, 0.7, nx, ny, not walls)
+HIGH2D_CASES = [
+    ("p_m9", 9, 4, 5, False, PRIMAL),
+    ("w_m9_dual", 9, 4, 4, True, DUAL),
+    ("p_m10", 10, 4, 4, False, DUAL),
+    ("w_m11_primal", 11, 3, 4, True, PRIMAL),
+    ("p_m12", 12, 4, 3, False, PRIMAL),
+    ("w_m12_dual", 12, 3, 3, True, DUAL),
+]
+
 
 def forcing_fn(l, s, x, t):
     import numpy as np
