@@ -30,6 +30,7 @@
 #pragma once
 
 #include <stdint.h>
+#include <stdio.h>
 
 #include <type_traits>
 
@@ -76,6 +77,34 @@ struct CellMapArgs {
 //     through a per-warp mbarrier (no consumer-side cp.async wait; measured
 //     2-6% slower than 0 at m = 4, 5: the drain then waits on the copies)
 #define HW_CM_PPREF 0
+#endif
+// HW_CM_DEBUG: race / bounds checking build (tools/race_stress.py; the pool
+// has no compute-sanitizer).  Every ring slot is poisoned with NaN between
+// its consumption and its refill, so a read of anything the producers did
+// not stage reaches the outputs as NaN; producers and consumers sleep for
+// random spans before each chunk, so orderings the barriers do not enforce
+// show up as run-to-run differences; global reads and writes are bounds-
+// checked against the field windows (trap on violation).
+#ifndef HW_CM_DEBUG
+#define HW_CM_DEBUG 0
+#endif
+#if HW_CM_DEBUG
+__device__ __forceinline__ unsigned cm_dbg_rand(unsigned a, unsigned b) {
+  unsigned x = (unsigned)clock64() ^ (a * 2654435761u) ^ (b * 40503u) ^ (blockIdx.x * 2246822519u);
+  x ^= x >> 13;
+  x *= 0x5bd1e995u;
+  x ^= x >> 15;
+  return x;
+}
+#define CM_DBG_CHECK(cond, what)                                                                  \
+  do {                                                                                            \
+    if (!(cond)) {                                                                                \
+      printf("cellmap debug: %s violated (block %d thread %d)\n", what, blockIdx.x, threadIdx.x); \
+      __trap();                                                                                   \
+    }                                                                                             \
+  } while (0)
+#else
+#define CM_DBG_CHECK(cond, what)
 #endif
 #ifndef HW_CM_SLEEP
 #define HW_CM_SLEEP 64  // producer back-off (ns) while its ring slot is busy and no slab is ready
@@ -317,9 +346,12 @@ __device__ __forceinline__ const double* cm_row(const Rows& R, int64_t s, int64_
   if (periodic) {
     while (s < 0) s += nx;
     while (s >= nx) s -= nx;
+    CM_DBG_CHECK(s >= R.row0 && s < R.row0 + R.nrows, "periodic source row inside the local window");
     return R.base + (s - R.row0) * rowlen;
   }
-  return R.base + ((s < 0 ? 0 : nx - 1) - R.row0) * rowlen;  // wall: mirror node, reflected later
+  const int64_t w = s < 0 ? 0 : nx - 1;  // wall: mirror node, reflected later
+  CM_DBG_CHECK(w >= R.row0 && w < R.row0 + R.nrows, "wall mirror row inside the local window");
+  return R.base + (w - R.row0) * rowlen;
 }
 
 // Tile geometry: target rows [tr0, tr0 + nvr) x columns [j0, j0 + nvc);
@@ -520,6 +552,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
           if (MODE == 2 || MODE == 3 || nv == 0) continue;
           double* o0 = a.out0 + cell0 * C::O0;
           const double* s0 = sl + t * NT * 64;
+          CM_DBG_CHECK(cell0 >= 0 && cell0 + nv <= a.ntrows * a.nty, "drained cells inside the target window");
           if (nv == 8) {  // full M-tile: fixed trip counts, loads batched 4 ahead of the stores
 #pragma unroll
             for (int k0 = 0; k0 < K0N; k0 += 4) {
@@ -622,6 +655,14 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
         break;
       }
       double* cb = smem + b * C::SBUF;
+#if HW_CM_DEBUG
+      {  // poison the slot (every consumer released it), then stage after a random delay
+        const double nanv = __longlong_as_double(0x7ff8dead00000000ll);
+        for (int i = pl; i < C::SBUF; i += NPL) cb[i] = nanv;
+        asm volatile("bar.sync 2, %0;\n" ::"n"(NPL) : "memory");
+        __nanosleep(cm_dbg_rand(g, tid) & 2047);
+      }
+#endif
       const int slot = ch * KC + e;  // input slot: field 0 in [0, K0), field 1 in [K0, 4 NK)
       const bool f1 = slot >= C::K0;
       const int eo = f1 ? slot - C::K0 : slot;
@@ -664,6 +705,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
         const int64_t rowlen = a.ny * pf;
         const double* src = (f1 ? a.f1.base : a.f0.base) + (t.s_first - a.f0.row0) * rowlen + (t.c_first + q0) * pf + eo;
         const int cstep = QL * pf;
+        CM_DBG_CHECK(t.s_first >= a.f0.row0 && t.s_first + TR < a.f0.row0 + a.f0.nrows, "interior tile rows local");
 #pragma unroll
         for (int r = 0; r <= TR; ++r) {
 #pragma unroll
@@ -799,6 +841,9 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
         if (C::CPREF) mbar_arrive_cp_async(&pready[warp]);  // the drain waits for these copies
       }
     }
+#if HW_CM_DEBUG
+    __nanosleep(cm_dbg_rand(g, tid) & 1023);
+#endif
     if (ch != 0) mbar_wait(&full[b], (g / NS) & 1);
     const double* cb = smem + b * C::SBUF;
     const double* wb = C::WRES ? smem + C::WRES0 + ch * KSC * NT * 32 : cb + C::CBUF;
