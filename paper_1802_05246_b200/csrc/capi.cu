@@ -1,5 +1,6 @@
 // extern "C" boundary (include/hermb200.h): argument checking, constant-table
 // construction and kernel dispatch.  Never throws across the ABI.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -95,6 +96,7 @@ static void check_bc_axis(const hw_axis_bc& b, int periodic) {
 // (device, scheme, m, dt, hx, hy, speed, stages).
 struct DevMap {
   double* wfrag = nullptr;
+  double* wleft = nullptr;
   int* ocode = nullptr;
   int* icode = nullptr;
   double* wdense = nullptr;  // [dout][din] class-major (simt2d.cuh)
@@ -119,6 +121,7 @@ constexpr size_t kMaxMaps = 48;
 
 static void free_map(DevMap& d) {
   cudaFree(d.wfrag);
+  cudaFree(d.wleft);
   cudaFree(d.ocode);
   cudaFree(d.icode);
   cudaFree(d.wdense);
@@ -143,8 +146,10 @@ static DevMap device_map(int scheme, int m, double dt, double hx, double hy, dou
       return g_maps.front().second;
     }
   const CellMap cm = build_cell_map(scheme, m, dt, hx, hy, speed, stages);
-  const int nk = cm_nk(scheme, m), nt = cm_nt(scheme, m);
-  std::vector<double> wf((size_t)nk * nt * 32, 0.0);
+  // fragment tiles: DMMA tiles (ntd) then SIMT tiles, whose columns are the
+  // left-over outputs of the hybrid classes (cellmap_shape.h)
+  const int nk = cm_nk(scheme, m), nt = cm_nt(scheme, m), ntd = cm_ntd(scheme, m), lc = cm_lc(scheme, m);
+  std::vector<double> wf((size_t)nk * ntd * 32, 0.0), wl((size_t)nk * lc * 4, 0.0);
   std::vector<int> oc((size_t)nt * 8, -1), ic((size_t)nk * 4, 0);
   // input slot -> map input e (field 0 entries, then field 1); -1 = pad slot
   const int p0 = cm.w_in[0] * cm.w_in[0], p1 = cm.w_in[1] * cm.w_in[1], k0 = cm_k0(scheme, m);
@@ -159,15 +164,24 @@ static DevMap device_map(int scheme, int m, double dt, double hx, double hy, dou
   }
   for (int c = 0; c < 4; ++c) {
     if (cm.ncls[c] != cm_ncls(scheme, m, c)) throw Error(HW_EINVAL, "internal: class size mismatch");
-    const int base = cm_ntbase(scheme, m, c);
-    for (int o = 0; o < cm.ncls[c]; ++o) oc[(size_t)(base + o / 8) * 8 + o % 8] = cm.code[c][o];
+    const int base = cm_ntbase(scheme, m, c), ntc = cm_ntc(scheme, m, c);
+    const int ndm = std::min(cm.ncls[c], 8 * ntc);  // outputs in DMMA tiles; the rest are SIMT columns
+    for (int o = 0; o < ndm; ++o) oc[(size_t)(base + o / 8) * 8 + o % 8] = cm.code[c][o];
     for (int ks = 0; ks < nk; ++ks)
-      for (int j = 0; j < cm_ntc(scheme, m, c); ++j)
+      for (int j = 0; j < ntc; ++j)
         for (int lane = 0; lane < 32; ++lane) {
           const int o = 8 * j + lane / 4, e = slot_e[4 * ks + lane % 4];
-          if (o < cm.ncls[c] && e >= 0)
-            wf[((size_t)ks * nt + base + j) * 32 + lane] = cm.w[c][(size_t)o * cm.din + e];
+          if (o < ndm && e >= 0) wf[((size_t)ks * ntd + base + j) * 32 + lane] = cm.w[c][(size_t)o * cm.din + e];
         }
+    for (int q = 0; q < cm_left(scheme, m, c); ++q) {
+      const int jcol = cm_lbase(scheme, m, c) + q, o = ndm + q;
+      oc[(size_t)(ntd + jcol / 8) * 8 + jcol % 8] = cm.code[c][o];
+      for (int ks = 0; ks < nk; ++ks)
+        for (int kk = 0; kk < 4; ++kk) {
+          const int e = slot_e[4 * ks + kk];
+          if (e >= 0) wl[((size_t)ks * lc + jcol) * 4 + kk] = cm.w[c][(size_t)o * cm.din + e];
+        }
+    }
   }
   // class-major dense maps for the SIMT kernel
   std::vector<double> wd((size_t)cm.dout * cm.din);
@@ -186,6 +200,9 @@ static DevMap device_map(int scheme, int m, double dt, double hx, double hy, dou
     cuda_check(cudaMemcpy(d.wdense, wd.data(), wd.size() * sizeof(double), cudaMemcpyHostToDevice), "upload wd");
     cuda_check(cudaMemcpy(d.dcode, dc.data(), dc.size() * sizeof(int), cudaMemcpyHostToDevice), "upload dcode");
     cuda_check(cudaMalloc(&d.wfrag, wf.size() * sizeof(double)), "cudaMalloc(wfrag)");
+    cuda_check(cudaMalloc(&d.wleft, std::max<size_t>(wl.size(), 1) * sizeof(double)), "cudaMalloc(wleft)");
+    if (!wl.empty())
+      cuda_check(cudaMemcpy(d.wleft, wl.data(), wl.size() * sizeof(double), cudaMemcpyHostToDevice), "upload wl");
     cuda_check(cudaMalloc(&d.ocode, oc.size() * sizeof(int)), "cudaMalloc(ocode)");
     cuda_check(cudaMalloc(&d.icode, ic.size() * sizeof(int)), "cudaMalloc(icode)");
     cuda_check(cudaMemcpy(d.wfrag, wf.data(), wf.size() * sizeof(double), cudaMemcpyHostToDevice), "upload wfrag");
@@ -309,6 +326,7 @@ static CellMapArgs cellmap_args(const Geo& g, const hw_geom2d* geom, const hw_ro
   a.f0 = to_rows(f0);
   a.f1 = f1 ? to_rows(f1) : a.f0;
   a.wfrag = dm.wfrag;
+  a.wleft = dm.wleft;
   a.ocode = dm.ocode;
   a.icode = dm.icode;
   a.nx = g.nx;

@@ -41,7 +41,8 @@ namespace hw {
 
 struct CellMapArgs {
   Rows f0, f1;                 // source fields (f1 unused when the scheme has one input)
-  const double* wfrag;         // [NK][NT][32] B fragments
+  const double* wfrag;         // [NK][NTD][32] B fragments of the DMMA tiles
+  const double* wleft;         // [NK][LC][4] weights of the SIMT columns (cellmap_shape.h hybrid tiles)
   const int* ocode;            // [NT][8] output field << 16 | offset in its record, -1 = padding
   const int* icode;            // [NK*4] (kx & 1) | (ky & 1) << 1 of each input slot
   const double* prev;          // kCons: previous level (may alias out0)
@@ -67,16 +68,6 @@ struct CellMapArgs {
 #endif
 #ifndef HW_CM_PDL
 #define HW_CM_PDL 1  // programmatic dependent launch between consecutive steps (A/B knob)
-#endif
-#ifndef HW_CM_PPREF
-// `previous` staging for the producer-drained conservative orders (A/B knob):
-// 0 = consumers copy it at the tile's last chunk and wait for it (round 1),
-// 1 = producers prefetch it one tile ahead (measured 0.69x at m = 5: the
-//     producers become the bottleneck),
-// 2 = consumers copy it at the last chunk and hand the wait to the drain
-//     through a per-warp mbarrier (no consumer-side cp.async wait; measured
-//     2-6% slower than 0 at m = 4, 5: the drain then waits on the copies)
-#define HW_CM_PPREF 0
 #endif
 // HW_CM_DEBUG: race / bounds checking build (tools/race_stress.py; the pool
 // has no compute-sanitizer).  Every ring slot is poisoned with NaN between
@@ -118,6 +109,8 @@ struct CMCfg {
   static constexpr int O0 = cm_wout(SCH, M, 0) * cm_wout(SCH, M, 0);
   static constexpr int O1 = cm_wout(SCH, M, 1) * cm_wout(SCH, M, 1);
   static constexpr int NK = cm_nk(SCH, M), NT = cm_nt(SCH, M);
+  static constexpr int NTD = cm_ntd(SCH, M), LC = cm_lc(SCH, M);  // DMMA tiles; SIMT columns (hybrid tiles)
+  static constexpr int WLN = NK * LC * 4;                          // resident SIMT weights (doubles)
   static constexpr int B1 = cm_ntbase(SCH, M, 1), B2 = cm_ntbase(SCH, M, 2), B3 = cm_ntbase(SCH, M, 3);
   static constexpr int KSC = cm_ksc();             // k-steps per chunk
   static constexpr int KC = 4 * KSC;               // input slots per chunk
@@ -153,26 +146,23 @@ struct CMCfg {
   // WRES: all NK k-steps of W stay resident in shared memory (loaded once per
   // CTA) instead of riding in every ring slot (cm_wres: where that measured
   // faster; W <= 40 KB).
-  static constexpr bool WRES = cm_wres(SCH, M) && NK * NT * 256 <= 40 * 1024;
-  static constexpr int WRESN = WRES ? NK * NT * 32 : 0;  // doubles
-  static constexpr int sbuf(int mt) { return (NW * mt / (TJ / 8) + 1) * (TJ + 1) * KCP + (WRES ? 0 : KSC * NT * 32); }
+  static constexpr bool WRES = cm_wres(SCH, M) && NK * NTD * 256 <= 40 * 1024;
+  static constexpr int WRESN = WRES ? NK * NTD * 32 : 0;  // doubles
+  static constexpr int sbuf(int mt) { return (NW * mt / (TJ / 8) + 1) * (TJ + 1) * KCP + (WRES ? 0 : KSC * NTD * 32); }
   // DIRECT: the consumers store their accumulators straight to HBM (no slab,
   // no producer drain).  SELF: each consumer warp drains its own slab
   // (fragment-order stores, record-order coalesced copy-out), no handoff.
   static constexpr bool DIRECT = cm_direct(SCH, M);
   static constexpr bool SELF = cm_self(SCH, M) && !DIRECT;
   static constexpr bool OWN = DIRECT || SELF;  // the consumers write HBM themselves
-  // `previous` of the producer-drained conservative orders reaches the drain
-  // through a per-warp mbarrier (pready) instead of a consumer cp.async wait:
-  // PPREF (HW_CM_PPREF 1) the producers stage it one tile ahead, CPREF (2)
-  // the consumers issue the copies at the tile's last chunk.
-  static constexpr bool PDRAIN = SCH == kCons && !(cm_direct(SCH, M) || (cm_self(SCH, M) && !cm_direct(SCH, M)));
-  static constexpr bool PPREF = HW_CM_PPREF == 1 && PDRAIN;
-  static constexpr bool CPREF = HW_CM_PPREF == 2 && PDRAIN;
-  static constexpr int NPR = (PPREF || CPREF) ? NW : 0;  // pready barriers
+  // kCons `previous`: per-lane registers (loaded at the tile's first chunk, subtracted
+  // in the epilogue) or a shared-memory slab (copied at the last chunk) — cm_prevreg
+  static constexpr bool PREVREG = SCH == kCons && cm_prevreg(SCH, M);
+  static constexpr bool PSMEM = SCH == kCons && !PREVREG;  // `previous` through a shared-memory slab
   static constexpr int tail(int mt) {
-    return WRESN * 8 + NW * ((DIRECT ? 0 : mt * NT * 64) + (SCH == kCons ? mt * 8 * O0 : 0)) * 8 + (8 * DO + 8 * NT) * 4 +
-           (2 * NSMAX + 2 * NW + NPR) * 8 + 64;
+    return (WRESN + WLN) * 8 + NW * ((DIRECT ? 0 : mt * NT * 64) + (PSMEM ? mt * 8 * O0 : 0)) * 8 +
+           (8 * DO + 8 * NT) * 4 +
+           (2 * NSMAX + 2 * NW) * 8 + 64;
   }
   static constexpr bool fits(int mt, int ns) { return ns * sbuf(mt) * 8 + tail(mt) <= SMEM_MAX; }
   // Ring depth: 4 slots only where they leave >= 56 KB of the SM's 256 KB
@@ -198,7 +188,7 @@ struct CMCfg {
   static constexpr int TR = NW * MT / (TJ / 8);    // target rows per tile
   static constexpr int NODES = (TR + 1) * (TJ + 1);
   static constexpr int CBUF = NODES * KCP;
-  static constexpr int WBUF = WRES ? 0 : KSC * NT * 32;
+  static constexpr int WBUF = WRES ? 0 : KSC * NTD * 32;
   static constexpr int SBUF = CBUF + WBUF;         // doubles per ring slot
   // bit ch: ring chunk ch lies inside one field whose record length is even
   // (so a multiple of 4: no padding slots) -> 16-byte staging copies
@@ -227,7 +217,7 @@ struct CMCfg {
 #else
   static constexpr int SWZ = SWZ0;
 #endif
-  static constexpr int PSLAB = SCH == kCons ? MT * 8 * O0 : 0;
+  static constexpr int PSLAB = PSMEM ? MT * 8 * O0 : 0;
   static constexpr int TAIL = tail(MT);
 #ifdef HW_CM_NS
   static constexpr int NS = cm_knob(SCH, M) && fits(MT, HW_CM_NS) ? HW_CM_NS :
@@ -241,12 +231,13 @@ struct CMCfg {
   static constexpr int NS = M == 4 ? 3 : (fits_soft(MT, 4) ? 4 : (fits(MT, 3) ? 3 : 2));
 #endif
   static constexpr int WRES0 = NS * SBUF;          // double offset of the resident W
-  static constexpr int EPI0 = WRES0 + WRESN;       // double offset of the slabs
+  static constexpr int WL0 = WRES0 + WRESN;        // double offset of the SIMT weights
+  static constexpr int EPI0 = WL0 + WLN;           // double offset of the slabs
   static constexpr int SMEM = NS * SBUF * 8 + TAIL;
 #ifdef HW_CM_PREB
-  static constexpr bool PREFETCH_B = cm_knob(SCH, M) ? HW_CM_PREB : NT <= 8;
+  static constexpr bool PREFETCH_B = cm_knob(SCH, M) ? HW_CM_PREB : NTD <= 8;
 #else
-  static constexpr bool PREFETCH_B = NT <= 8;      // W fragments double-buffered in registers too
+  static constexpr bool PREFETCH_B = NTD <= 8;     // W fragments double-buffered in registers too
 #endif
 };
 
@@ -270,7 +261,25 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void mbar_arrive_cp_async(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
+// HW_CM_WAITHINT > 0: try_wait with a suspend-time hint (ns), so a waiting
+// warp is parked by the hardware instead of spinning on issue slots (A/B knob).
+#ifndef HW_CM_WAITHINT
+#define HW_CM_WAITHINT 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+#if HW_CM_WAITHINT > 0
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "n"(HW_CM_WAITHINT)
+      : "memory");
+#else
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
@@ -282,6 +291,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+#endif
 }
 
 // Non-blocking probe of a phase (warp-uniform when called by one lane and
@@ -394,8 +404,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
   uint64_t* empty = bars + C::NSMAX;      // [NS] consumers -> producers: ring slot consumed
   uint64_t* sfull = bars + 2 * C::NSMAX;  // [NW] consumer w -> producer: output slab written
   uint64_t* sempty = sfull + NW;          // [NW] producer -> consumer w: output slab drained
-  uint64_t* pready = sempty + NW;         // [NPR] producer lanes' `previous` copies of warp w's next tile landed
-  int* s_tile = reinterpret_cast<int*>(pready + C::NPR);  // [QT] tile id of this CTA's k-th tile (in the tail's slack)
+  int* s_tile = reinterpret_cast<int*>(sempty + NW);  // [QT] tile id of this CTA's k-th tile (in the tail's slack)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   // Inverse fragment map: output q of an M-tile's records, laid out
@@ -411,6 +420,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       s_inv[q] = (nt * 32 + ((r * 4 + col / 2 + C::SWZ * nt) & 31)) * 2 + col % 2;
     }
   }
+  for (int i = tid; i < C::WLN; i += blockDim.x) smem[C::WL0 + i] = a.wleft[i];  // (not step data: before the PDL wait)
   if (tid == 0) {
     s_tile[0] = blockIdx.x;
     for (int b = 0; b < NS; ++b) {
@@ -421,7 +431,6 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       mbar_init(&sfull[w], 1);
       mbar_init(&sempty[w], 1);
     }
-    for (int w = 0; w < C::NPR; ++w) mbar_init(&pready[w], 32);  // one cp.async arrive per producer lane
   }
   __syncthreads();
 #if HW_CM_PDL
@@ -449,8 +458,8 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
   // ends the CTA's sequence; the last CTA to make that claim zeroes the
   // counters for the next launch.  Null a.sched: static round robin.
   static_assert(C::NS + 2 <= C::QT, "tile-id ring shorter than the tiles in flight");
-  static_assert((2 * C::NSMAX + 2 * NW + C::NPR) * 8 + (8 * C::DO + 8 * NT) * 4 + 4 * C::QT + 4 <=
-                    (2 * C::NSMAX + 2 * NW + C::NPR) * 8 + (8 * C::DO + 8 * NT) * 4 + 64,
+  static_assert((2 * C::NSMAX + 2 * NW) * 8 + (8 * C::DO + 8 * NT) * 4 + 4 * C::QT + 4 <=
+                    (2 * C::NSMAX + 2 * NW) * 8 + (8 * C::DO + 8 * NT) * 4 + 64,
                 "s_tile must fit the tail's slack");
 
   auto tile_geo = [&](int tile) {
@@ -506,30 +515,6 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
 #pragma unroll
       for (int k = 0; k < K1N; ++k) inv[K0N + k] = lane + 32 * k < 8 * C::O1 ? s_inv[8 * C::O0 + lane + 32 * k] : 0;
     }
-    // PPREF: stage `previous` of consumer warp w's kt-th tile into its slab
-    // (its id is published: kt <= this CTA's staged tile count); every lane
-    // arrives on pready[w] once its own copies have landed.
-    auto prefetch_prev = [&](int w, int kt) {
-      if constexpr (C::PPREF) {
-        const int tile = s_tile[kt % C::QT];
-        if (tile < ntiles && MODE != 2 && MODE != 3) {
-          const CMTile tg = tile_geo(tile);
-          double* pv = pslabs + w * C::PSLAB;
-#pragma unroll
-          for (int t = 0; t < MT; ++t) {
-            int64_t cell0;
-            const int nv = mtile(tg, w, t, cell0);
-            const double* p = a.prev + cell0 * C::O0;
-            for (int q = lane; q < nv * C::O0; q += 32) cm_cp_async8(pv + t * 8 * C::O0 + q, p + q);
-          }
-        }
-        mbar_arrive_cp_async(&pready[w]);
-      }
-    };
-    if constexpr (C::PPREF) {
-#pragma unroll
-      for (int j = 0; j < NW / C::NPW; ++j) prefetch_prev(pw + C::NPW * j, 0);
-    }
     auto try_drain = [&]() {
       bool any = false;
       if constexpr (!C::OWN) {  // (DIRECT / SELF: the consumers store their own outputs)
@@ -537,9 +522,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       for (int j = 0; j < NW / C::NPW; ++j) {
         const int w = pw + C::NPW * j;
         if (dk[j] >= ktot) continue;
-        int ready = 0;
-        if (lane == 0)
-          ready = (int)mbar_test(&sfull[w], dk[j] & 1) && (C::NPR == 0 || mbar_test(&pready[w], dk[j] & 1));
+        int ready = lane == 0 ? (int)mbar_test(&sfull[w], dk[j] & 1) : 0;
         ready = __shfl_sync(0xffffffffu, ready, 0);
         if (!ready) continue;
         const CMTile tg = tile_geo(s_tile[dk[j] % C::QT]);
@@ -562,7 +545,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
                 const int q = lane + 32 * (k0 + u);
                 if (k0 + u < K0N && q < 8 * C::O0) {
                   v[u] = s0[INVREG ? inv[INVREG ? k0 + u : 0] : s_inv[q]];
-                  if (SCH == kCons) v[u] -= pl0[t * 8 * C::O0 + q];  // conservative.py:136
+                  if (C::PSMEM) v[u] -= pl0[t * 8 * C::O0 + q];  // conservative.py:136
                 }
               }
 #pragma unroll
@@ -591,7 +574,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
             }
           } else {
             for (int q = lane; q < nv * C::O0; q += 32)
-              o0[q] = SCH == kCons ? s0[s_inv[q]] - pl0[t * 8 * C::O0 + q] : s0[s_inv[q]];
+              o0[q] = C::PSMEM ? s0[s_inv[q]] - pl0[t * 8 * C::O0 + q] : s0[s_inv[q]];
             if (C::O1 > 0) {
               double* o1 = a.out1 + cell0 * C::O1;
               for (int q = lane; q < nv * C::O1; q += 32) o1[q] = s0[s_inv[8 * C::O0 + q]];
@@ -601,9 +584,6 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
         __syncwarp();
         if (lane == 0) mbar_arrive(&sempty[w]);
         ++dk[j];
-        // this lane's reads of the slab's `previous` entries are done (their
-        // values went to HBM above): refill them for the warp's next tile
-        prefetch_prev(w, dk[j]);
         any = true;
       }
       }
@@ -758,13 +738,13 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       // W fragments of the chunk (contiguous, 16-byte aligned)
       const int nks = (C::NK - ch * KSC) < KSC ? (C::NK - ch * KSC) : KSC;
       if (!C::WRES) {
-        const double* wsrc = a.wfrag + ch * KSC * NT * 32;
+        const double* wsrc = a.wfrag + ch * KSC * C::NTD * 32;
         double* wb = cb + C::CBUF;
 #pragma unroll 1
-        for (int i = pl; i < nks * NT * 16; i += NPL) cm_cp_async16(wb + 2 * i, wsrc + 2 * i);
+        for (int i = pl; i < nks * C::NTD * 16; i += NPL) cm_cp_async16(wb + 2 * i, wsrc + 2 * i);
       } else if (g == 0) {  // the whole W once; stage 0's cp.async arrive covers it
 #pragma unroll 1
-        for (int i = pl; i < C::NK * NT * 16; i += NPL) cm_cp_async16(smem + C::WRES0 + 2 * i, a.wfrag + 2 * i);
+        for (int i = pl; i < C::NK * C::NTD * 16; i += NPL) cm_cp_async16(smem + C::WRES0 + 2 * i, a.wfrag + 2 * i);
       }
       mbar_arrive(&full[b]);           // orders this lane's plain shared stores
       mbar_arrive_cp_async(&full[b]);  // fires when this lane's copies have landed
@@ -811,6 +791,9 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
   for (int t = 0; t < MT; ++t)
 #pragma unroll
     for (int n = 0; n < NT; ++n) acc[t][n][0] = acc[t][n][1] = 0.0;
+  constexpr int LC = C::LC, NTD = C::NTD;
+  double part[MT][LC > 0 ? LC : 1];  // SIMT columns: this lane's partial sums over its input slots
+  double pvr[C::PREVREG ? MT : 1][C::PREVREG ? NT : 1][2];  // PREVREG: `previous` at this lane's accumulator slots
 
   int ch = 0, k = 0;  // k = this warp's tile count
   CMTile cg;
@@ -822,6 +805,25 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       const int tile = s_tile[k % C::QT];
       if (tile >= ntiles) break;
       cg = tile_geo(tile);
+      if constexpr (C::PREVREG) {
+        // `previous` of this lane's accumulator slots (cell r = lane / 4 of each
+        // M-tile, columns 2 (lane & 3), +1 of each n-tile): plain loads issued
+        // now land while the tile's DMMAs run; used in the epilogue.  In place
+        // is safe: only this tile's epilogue writes these records, later.
+#pragma unroll
+        for (int t = 0; t < MT; ++t) {
+          int64_t cell0;
+          const int nv = mtile(cg, warp, t, cell0);
+          const double* pc = a.prev + (cell0 + (lane >> 2)) * C::O0;
+#pragma unroll
+          for (int n = 0; n < NT; ++n)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int code = s_ocode[n * 8 + 2 * (lane & 3) + i];
+              pvr[t][n][i] = (code >= 0 && (lane >> 2) < nv) ? pc[code & 0xffff] : 0.0;
+            }
+        }
+      }
     }
     if (ch == NCH - 1) {
       // The tile's last chunk: the previous tile's slab must be drained before
@@ -829,7 +831,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       // records are staged — contiguous, with cp.async, landing under the
       // last chunk's DMMAs).
       if (!C::OWN && k >= 1) mbar_wait(&sempty[warp], (k - 1) & 1);
-      if (SCH == kCons && !C::PPREF) {  // (CPREF: the drain, not this warp, waits for the copies)
+      if (C::PSMEM) {
         double* pv = pslabs + warp * C::PSLAB;
 #pragma unroll
         for (int t = 0; t < MT; ++t) {
@@ -838,7 +840,6 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
           const double* p = a.prev + cell0 * C::O0;
           for (int q = lane; q < nv * C::O0; q += 32) cm_cp_async8(pv + t * 8 * C::O0 + q, p + q);
         }
-        if (C::CPREF) mbar_arrive_cp_async(&pready[warp]);  // the drain waits for these copies
       }
     }
 #if HW_CM_DEBUG
@@ -846,7 +847,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
 #endif
     if (ch != 0) mbar_wait(&full[b], (g / NS) & 1);
     const double* cb = smem + b * C::SBUF;
-    const double* wb = C::WRES ? smem + C::WRES0 + ch * KSC * NT * 32 : cb + C::CBUF;
+    const double* wb = C::WRES ? smem + C::WRES0 + ch * KSC * NTD * 32 : cb + C::CBUF;
     // One chunk of NKS k-steps, software-pipelined: the shared-memory
     // operands of k-step ks+1 (corner values; W fragments when registers
     // allow) are loaded before the DMMAs of k-step ks issue.  FIRST: the
@@ -858,7 +859,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       // raw[.][r] = the two y-corners of staged row trl0 + r (row r + 1 of
       // M-tile r is row 0 of M-tile r + 1: MT + 1 rows feed MT M-tiles)
       double raw[2][MT + 1][2];
-      double bb[PREB ? 2 : 1][NT];
+      double bb[PREB ? 2 : 1][NTD];
       const int trl0 = (warp / (TJ / 8)) * MT, tc = (warp % (TJ / 8)) * 8;
       const double* pbase = cb + (trl0 * (TJ + 1) + tc + (lane >> 2)) * KCP + (lane & 3);
       auto load = [&](const int ks, const int slot) {
@@ -869,9 +870,9 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
           raw[slot][r][1] = p[KCP];
         }
         if (PREB) {
-          const double* wk = wb + ks * NT * 32 + lane;
+          const double* wk = wb + ks * NTD * 32 + lane;
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) bb[PREB ? slot : 0][nt] = wk[nt * 32];
+          for (int nt = 0; nt < NTD; ++nt) bb[PREB ? slot : 0][nt] = wk[nt * 32];
         }
       };
       load(0, 0);
@@ -895,9 +896,22 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
           A[t][2] = am + bm;  // class (1,0)
           A[t][3] = am - bm;  // class (1,1)
         }
-        const double* wk = wb + ks * NT * 32 + lane;
+        const double* wk = wb + ks * NTD * 32 + lane;
+        if constexpr (LC > 0) {
+          // SIMT columns: W_c[o][slot] for this lane's slot (4 distinct per warp: one wavefront)
+          const double* wl = smem + C::WL0 + step * LC * 4 + (lane & 3);
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
+          for (int j = 0; j < LC; ++j) {
+            const double w = wl[j * 4];
+#pragma unroll
+            for (int t = 0; t < MT; ++t) {
+              const double av = A[t][cm_lclass(SCH, M, j)];
+              part[t][j] = (FIRST && ks == 0) ? w * av : fma(w, av, part[t][j]);
+            }
+          }
+        }
+#pragma unroll
+        for (int nt = 0; nt < NTD; ++nt) {
           const int c = nt < C::B1 ? 0 : (nt < C::B2 ? 1 : (nt < C::B3 ? 2 : 3));  // parity class of tile nt
           const double bf = PREB ? bb[PREB ? cur : 0][nt] : wk[nt * 32];
 #pragma unroll
@@ -926,11 +940,48 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[b]);  // ring slot b may be refilled
+    if constexpr (LC > 0) {
+      if (ch == NCH - 1) {
+        // the four lanes of a cell (lane & 3 = its input slots) sum their partials;
+        // lane 4 r + q then holds SIMT columns 2 q, 2 q + 1 of each SIMT tile (fragment layout)
+#pragma unroll
+        for (int t = 0; t < MT; ++t) {
+#pragma unroll
+          for (int j = 0; j < LC; ++j) {
+            double v = part[t][j];
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            part[t][j] = v;
+          }
+#pragma unroll
+          for (int s2 = 0; s2 < C::NT - NTD; ++s2)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              double v = 0.0;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int j = 8 * s2 + 2 * q + i;
+                if (j < LC && (lane & 3) == q) v = part[t][j < LC ? j : 0];
+              }
+              acc[t][NTD + s2][i] = v;
+            }
+        }
+      }
+    }
 
+    if (C::PREVREG && ch == NCH - 1) {  // conservative.py:136: new = 2 WT I(cur) - previous
+#pragma unroll
+      for (int t = 0; t < MT; ++t)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          acc[t][n][0] -= pvr[t][n][0];
+          acc[t][n][1] -= pvr[t][n][1];
+        }
+    }
     if (ch == NCH - 1 && C::DIRECT) {
       // Epilogue straight to HBM: lane 4 r + j stores outputs 2 j, 2 j + 1 of
       // every n-tile for cell r of each M-tile.
-      if (SCH == kCons) asm volatile("cp.async.wait_all;\n" ::: "memory");  // `previous` landed
+      if (C::PSMEM) asm volatile("cp.async.wait_all;\n" ::: "memory");  // `previous` landed
       const double* pv = pslabs + warp * C::PSLAB;
       const int r = lane >> 2;
 #pragma unroll
@@ -950,7 +1001,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
             if (code >> 16)
               d1[o] = acc[t][n][i];
             else
-              d0[o] = SCH == kCons ? acc[t][n][i] - pv[t * 8 * C::O0 + r * C::O0 + o] : acc[t][n][i];
+              d0[o] = C::PSMEM ? acc[t][n][i] - pv[t * 8 * C::O0 + r * C::O0 + o] : acc[t][n][i];
           }
       }
       __syncwarp();
@@ -963,7 +1014,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
         for (int n = 0; n < NT; ++n)
           *reinterpret_cast<double2*>(slab + t * NT * 64 + (n * 32 + ((lane + C::SWZ * n) & 31)) * 2) =
               make_double2(acc[t][n][0], acc[t][n][1]);
-      if (SCH == kCons && !C::PPREF && !C::CPREF) asm volatile("cp.async.wait_all;\n" ::: "memory");  // `previous` landed
+      if (C::PSMEM) asm volatile("cp.async.wait_all;\n" ::: "memory");  // `previous` landed
       __syncwarp();
       if constexpr (C::SELF) {
         // drain it ourselves: record order, consecutive lanes on consecutive doubles
@@ -976,7 +1027,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
           const double* s0 = slab + t * NT * 64;
           double* o0 = a.out0 + cell0 * C::O0;
           for (int q = lane; q < nv * C::O0; q += 32)
-            o0[q] = SCH == kCons ? s0[s_inv[q]] - pv[t * 8 * C::O0 + q] : s0[s_inv[q]];
+            o0[q] = C::PSMEM ? s0[s_inv[q]] - pv[t * 8 * C::O0 + q] : s0[s_inv[q]];
           if (C::O1 > 0) {
             double* o1 = a.out1 + cell0 * C::O1;
             for (int q = lane; q < nv * C::O1; q += 32) o1[q] = s0[s_inv[8 * C::O0 + q]];

@@ -10,6 +10,17 @@ enum Scheme : int { kDiss = 0, kCons = 1, kBoot = 2 };
 constexpr int cm_win(int sch, int m, int f) { return f == 0 ? m + 1 : (sch == 0 ? m : (sch == 2 ? m + 1 : 0)); }
 constexpr int cm_wout(int sch, int m, int f) { return f == 0 ? m + 1 : (sch == 0 ? m : 0); }
 
+// (A/B knob filter, as cm_knob below)
+constexpr bool cm_knob_h(int sch, int m) {
+#ifdef HW_CM_KNOB_M
+  if (m != HW_CM_KNOB_M) return false;
+#endif
+#ifdef HW_CM_KNOB_SCH
+  if (sch != HW_CM_KNOB_SCH) return false;
+#endif
+  return sch >= 0 && m >= 0;
+}
+
 // number of k in [0, w) with k % 2 == p
 constexpr int cm_cnt_par(int w, int p) { return w > p ? (w - 1 - p) / 2 + 1 : 0; }
 
@@ -24,17 +35,61 @@ constexpr int cm_ncls(int sch, int m, int c) {
          cm_cnt_par(cm_wout(sch, m, 1), c >> 1) * cm_cnt_par(cm_wout(sch, m, 1), c & 1);
 }
 
-// 8-wide output tiles of class c (DMMA m8n8k4: N = 8) and their prefix sums
-constexpr int cm_ntc(int sch, int m, int c) { return (cm_ncls(sch, m, c) + 7) / 8; }
+// Hybrid tiles.  A class's outputs fill 8-wide DMMA n-tiles (m8n8k4: N = 8);
+// where class c's remainder r_c = n_c mod 8 is in the class mask cm_lmask,
+// those r_c outputs are computed on the CUDA cores instead of padding a
+// whole n-tile: each lane accumulates W_c[o][e] G^c[e] over its own input
+// slots (the A fragment it already holds) and the four lanes of a cell sum
+// by shuffles.  The left-over outputs of all masked classes form the columns
+// of extra "SIMT" tiles laid out like DMMA fragments, so the epilogue is
+// unchanged.  (Pipe cost per M-tile and k-step: a padded DMMA tile 4 clocks
+// of the SM's FP64 datapath, r_c SIMT columns r_c / 2 clocks.)
+constexpr int cm_lmask(int sch, int m) {
+#ifdef HW_CM_LMASK
+  if (cm_knob_h(sch, m)) return HW_CM_LMASK;
+#endif
+  // measured (profiles/ab_r02_kernel_knobs.txt): cons m = 5 (+7%); diss m = 4 -2% (0x6) / -7% (0xf): off
+  return (sch == 1 && m == 5) ? 0xf : 0;
+}
+constexpr int cm_rem(int sch, int m, int c) { return cm_ncls(sch, m, c) % 8; }
+constexpr int cm_left(int sch, int m, int c) { return (cm_lmask(sch, m) >> c & 1) ? cm_rem(sch, m, c) : 0; }
+// DMMA n-tiles of class c and their prefix sums
+constexpr int cm_ntc(int sch, int m, int c) {
+  return cm_left(sch, m, c) ? cm_ncls(sch, m, c) / 8 : (cm_ncls(sch, m, c) + 7) / 8;
+}
 constexpr int cm_ntbase(int sch, int m, int c) {  // non-recursive: folds inside unrolled device loops
   return (c > 0 ? cm_ntc(sch, m, 0) : 0) + (c > 1 ? cm_ntc(sch, m, 1) : 0) + (c > 2 ? cm_ntc(sch, m, 2) : 0) +
          (c > 3 ? cm_ntc(sch, m, 3) : 0);
 }
-constexpr int cm_nt(int sch, int m) { return cm_ntbase(sch, m, 4); }
+constexpr int cm_ntd(int sch, int m) { return cm_ntbase(sch, m, 4); }  // DMMA tiles
+// SIMT columns (left-over outputs, class 0's first) and SIMT tiles
+constexpr int cm_lbase(int sch, int m, int c) {
+  return (c > 0 ? cm_left(sch, m, 0) : 0) + (c > 1 ? cm_left(sch, m, 1) : 0) + (c > 2 ? cm_left(sch, m, 2) : 0) +
+         (c > 3 ? cm_left(sch, m, 3) : 0);
+}
+constexpr int cm_lc(int sch, int m) { return cm_lbase(sch, m, 4); }
+constexpr int cm_lclass(int sch, int m, int j) {  // class of SIMT column j
+  return j < cm_lbase(sch, m, 1) ? 0 : (j < cm_lbase(sch, m, 2) ? 1 : (j < cm_lbase(sch, m, 3) ? 2 : 3));
+}
+constexpr int cm_nts(int sch, int m) { return (cm_lc(sch, m) + 7) / 8; }
+// all fragment-layout tiles (accumulators, epilogue): DMMA, then SIMT
+constexpr int cm_nt(int sch, int m) { return cm_ntd(sch, m) + cm_nts(sch, m); }
 
-// parity class that output tile nt belongs to
+// parity class that DMMA output tile nt belongs to
 constexpr int cm_class_of_tile(int sch, int m, int nt) {
   return nt < cm_ntbase(sch, m, 1) ? 0 : (nt < cm_ntbase(sch, m, 2) ? 1 : (nt < cm_ntbase(sch, m, 3) ? 2 : 3));
+}
+
+// Conservative scheme: `previous` loaded into registers at the tile's first
+// chunk and subtracted from the accumulators (1), or copied into a
+// shared-memory slab at the last chunk (0): registers measured +2% at m = 5,
+// +12% at m = 6; the slab stays where the registers run out (m = 3: -27%,
+// m = 8: -55%) (profiles/ab_r02_kernel_knobs.txt).
+constexpr bool cm_prevreg(int sch, int m) {
+#ifdef HW_CM_PREVREG
+  if (cm_knob_h(sch, m)) return HW_CM_PREVREG;
+#endif
+  return sch == 1 && (m == 5 || m == 6);
 }
 
 // Input slots: each field's entries padded to a multiple of 4 (a 4-deep
