@@ -97,6 +97,9 @@ __device__ __forceinline__ unsigned cm_dbg_rand(unsigned a, unsigned b) {
 #else
 #define CM_DBG_CHECK(cond, what)
 #endif
+#ifndef HW_CM_DCODE
+#define HW_CM_DCODE 1  // direct epilogue: per-lane output codes resolved once, branch-free stores (A/B knob)
+#endif
 #ifndef HW_CM_SLEEP
 #define HW_CM_SLEEP 64  // producer back-off (ns) while its ring slot is busy and no slab is ready
 #endif
@@ -786,6 +789,15 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
     kxbits |= (unsigned long long)(code & 1) << st;
     kybits |= (unsigned long long)((code >> 1) & 1) << st;
   }
+#if HW_CM_DCODE
+  int dcode[C::DIRECT ? NT : 1][2];  // DIRECT epilogue: this lane's output codes (field << 16 | offset, -1 pad)
+  if constexpr (C::DIRECT) {
+#pragma unroll
+    for (int n = 0; n < NT; ++n)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) dcode[n][i] = s_ocode[n * 8 + 2 * (lane & 3) + i];
+  }
+#endif
   double acc[MT][NT][2];
 #pragma unroll
   for (int t = 0; t < MT; ++t)
@@ -991,6 +1003,19 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
         if (MODE == 3 || r >= nv) continue;
         double* d0 = a.out0 + (cell0 + r) * C::O0;
         double* d1 = C::O1 > 0 ? a.out1 + (cell0 + r) * C::O1 : nullptr;
+#if HW_CM_DCODE
+        // branch-free: this lane's destinations were resolved once (dcode)
+#pragma unroll
+        for (int n = 0; n < NT; ++n)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int code = dcode[n][i];
+            double* base = (C::O1 > 0 && (code >> 16) > 0) ? d1 : d0;
+            double v = acc[t][n][i];
+            if (C::PSMEM) v -= (code >= 0 && (code >> 16) == 0) ? pv[t * 8 * C::O0 + r * C::O0 + (code & 0xffff)] : 0.0;
+            if (code >= 0) base[code & 0xffff] = v;
+          }
+#else
 #pragma unroll
         for (int n = 0; n < NT; ++n)
 #pragma unroll
@@ -1003,6 +1028,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
             else
               d0[o] = C::PSMEM ? acc[t][n][i] - pv[t * 8 * C::O0 + r * C::O0 + o] : acc[t][n][i];
           }
+#endif
       }
       __syncwarp();
     } else if (ch == NCH - 1) {
