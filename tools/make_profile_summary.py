@@ -79,16 +79,17 @@ def full_capture(rep):
 
 def main():
     launches_csv, rep, key = sys.argv[1], sys.argv[2], sys.argv[3]
-    rnd = sys.argv[4] if len(sys.argv) > 4 else "r01"
+    rnd = sys.argv[4] if len(sys.argv) > 4 else "r02"
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     summ = json.load(open(path)) if os.path.exists(path) else {}
     summ["round"] = rnd
     summ["how"] = ("launch list: ncu --metrics gpu__time_duration.sum --clock-control none -c 400 on "
-                   "`python bench.py --steps 3 --warmup 3 --no-sweep --no-e2e --no-cpu --no-c3`; full capture: "
+                   "`python bench.py --steps 3 --warmup 3 --no-sweep --no-e2e --no-cpu --no-c3 --no-c5`; full capture: "
                    "ncu --set full --clock-control none -k regex:cellmap -s 3 -c 1 on the same command "
                    "(tools/gpu_bench.sh).  Cold-cache, serialised: shares, not absolutes.")
     summ.setdefault("launches", {})[key] = full_capture(rep)
-    summ.setdefault("launch_list", {})[key] = launch_list(launches_csv)
+    if launches_csv != "-":
+        summ.setdefault("launch_list", {})[key] = launch_list(launches_csv)
     with open(path, "w") as f:
         json.dump(summ, f, indent=1)
     print(json.dumps(summ["launches"][key], indent=1))
