@@ -826,17 +826,13 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
         for (int t = 0; t < MT; ++t) {
           int64_t cell0;
           const int nv = mtile(cg, warp, t, cell0);
-          if (nv == 0) continue;  // (warp-uniform)
-          // unconditional loads from a clamped in-window address; the validity
-          // select happens in the epilogue, so nothing waits on them until then
-          const int r = (lane >> 2) < nv ? (lane >> 2) : 0;
-          const double* pc = a.prev + (cell0 + r) * C::O0;
+          const double* pc = a.prev + (cell0 + (lane >> 2)) * C::O0;
 #pragma unroll
           for (int n = 0; n < NT; ++n)
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
               const int code = s_ocode[n * 8 + 2 * (lane & 3) + i];
-              pvr[t][n][i] = pc[code >= 0 ? (code & 0xffff) : 0];
+              pvr[t][n][i] = (code >= 0 && (lane >> 2) < nv) ? pc[code & 0xffff] : 0.0;
             }
         }
       }
@@ -987,17 +983,12 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
 
     if (C::PREVREG && ch == NCH - 1) {  // conservative.py:136: new = 2 WT I(cur) - previous
 #pragma unroll
-      for (int t = 0; t < MT; ++t) {
-        int64_t cell0;
-        const int nv = mtile(cg, warp, t, cell0);
+      for (int t = 0; t < MT; ++t)
 #pragma unroll
-        for (int n = 0; n < NT; ++n)
-#pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const bool ok = s_ocode[n * 8 + 2 * (lane & 3) + i] >= 0 && (lane >> 2) < nv;
-            acc[t][n][i] -= ok ? pvr[t][n][i] : 0.0;
-          }
-      }
+        for (int n = 0; n < NT; ++n) {
+          acc[t][n][0] -= pvr[t][n][0];
+          acc[t][n][1] -= pvr[t][n][1];
+        }
     }
     if (ch == NCH - 1 && C::DIRECT) {
       // Epilogue straight to HBM: lane 4 r + j stores outputs 2 j, 2 j + 1 of
