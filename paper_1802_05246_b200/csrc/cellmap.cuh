@@ -115,10 +115,12 @@ struct CMCfg {
   static constexpr int NTD = cm_ntd(SCH, M), LC = cm_lc(SCH, M);  // DMMA tiles; SIMT columns (hybrid tiles)
   static constexpr int WLN = NK * LC * 4;                          // resident SIMT weights (doubles)
   static constexpr int B1 = cm_ntbase(SCH, M, 1), B2 = cm_ntbase(SCH, M, 2), B3 = cm_ntbase(SCH, M, 3);
-  static constexpr int KSC = cm_ksc();             // k-steps per chunk
+  static constexpr int KSC = cm_ksc(SCH, M);       // k-steps per chunk
   static constexpr int KC = 4 * KSC;               // input slots per chunk
   static constexpr int NCH = (NK + KSC - 1) / KSC; // chunks per tile
-  static constexpr int KCP = 20;                   // staged doubles per node (= 4 mod 16: conflict-free)
+  // staged doubles per node: = +-4 mod 16 keeps the fragment reads of 8 nodes x 4 slots conflict-free
+  static constexpr int KCP = KC <= 12 ? 12 : 20;
+  static_assert(KC <= KCP && (KCP % 16 == 4 || KCP % 16 == 12), "ring node stride");
   static constexpr int NW = cm_nw(SCH, M);         // consumer warps (a multiple of 4)
 #ifdef HW_CM_NPW
   static constexpr int NPW = HW_CM_NPW;
@@ -231,7 +233,8 @@ struct CMCfg {
   static constexpr int NS = deepest(NSMAX);
 #else
   // (m = 4: 3 slots measured faster than 4 — conservative 5%, dissipative 0.5-0.8%; tools/gpu_ab.sh)
-  static constexpr int NS = M == 4 ? 3 : (fits_soft(MT, 4) ? 4 : (fits(MT, 3) ? 3 : 2));
+  static constexpr int NS = cm_ns(SCH, M) && fits(MT, cm_ns(SCH, M)) ? cm_ns(SCH, M) :
+      (M == 4 ? 3 : (fits_soft(MT, 4) ? 4 : (fits(MT, 3) ? 3 : 2)));
 #endif
   static constexpr int WRES0 = NS * SBUF;          // double offset of the resident W
   static constexpr int WL0 = WRES0 + WRESN;        // double offset of the SIMT weights
@@ -495,6 +498,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
     constexpr int NQ = (TJ + QL) / QL;  // node columns per lane (ceil((TJ+1)/QL))
     const int pl = tid - 32 * NW, pw = warp - NW;
     const int e = pl % KC, q0 = pl / KC;
+    const bool active = q0 < QL;  // (KC not dividing the producer lanes: the last few lanes stage nothing)
 
     // Output drain for consumer warps pw and pw + NPW: slab -> HBM, coalesced.
     int ktot = 0x7fffffff;  // this CTA's tile count, once its last claim has come back
@@ -658,10 +662,10 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       if (MODE != 1 && interior && (C::WIDE >> ch & 1u) && base_al16) {
         // interior tile, chunk inside one field of even record length (no
         // padding slots): 16-byte L2-only copies of slot pairs, lane -> (pair
-        // pl % 8, node pl / 8); slots beyond the last k-step are never read
-        constexpr int QW = NPL / 8, NQW = (TJ + QW) / QW;
-        const int e2 = 2 * (pl % 8), qw = pl / 8;
-        if (ch * KC + e2 < 4 * C::NK) {
+        // pl % (KC/2), node pl / (KC/2)); slots beyond the last k-step are never read
+        constexpr int PAIRS = KC / 2, QW = NPL / PAIRS, NQW = (TJ + QW) / QW;
+        const int e2 = 2 * (pl % PAIRS), qw = pl / PAIRS;
+        if (qw < QW && ch * KC + e2 < 4 * C::NK) {
           const bool fw = ch * KC >= C::K0;
           const int pf = fw ? C::P1 : C::P0;
           const int64_t rowlen = a.ny * pf;
@@ -676,6 +680,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
             src += rowlen;
           }
         }
+      } else if (!active) {
       } else if (pad) {
 #pragma unroll 1
         for (int r = 0; r <= TR; ++r)

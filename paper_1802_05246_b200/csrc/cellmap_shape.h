@@ -114,11 +114,18 @@ constexpr bool cm_knob(int sch, int m) {
 }
 
 // The kernel's staging unit: k-steps per ring chunk.
+constexpr int cm_ksc(int sch, int m) {
 #ifdef HW_CM_KSC
-constexpr int cm_ksc() { return HW_CM_KSC; }
-#else
-constexpr int cm_ksc() { return 4; }
+  if (cm_knob_h(sch, m)) return HW_CM_KSC;
 #endif
+  // conservative m = 5 (NK = 9): three 3-k-step chunks instead of 4 + 4 + 1, with the smaller ring
+  // slots (node stride 12) allowing a 5-deep ring: 1.23x; conservative m = 6 likewise 1.06x
+  // (profiles/ab_r02_kernel_knobs.txt: 2-k-step chunks and 3-k-step chunks elsewhere measured slower)
+  return (sch == 1 && (m == 5 || m == 6)) ? 3 : 4;
+}
+
+// Ring depth override (0 = the shared-memory rule in CMCfg).
+constexpr int cm_ns(int sch, int m) { return (sch == 1 && (m == 5 || m == 6)) ? 5 : 0; }
 
 // Consumer warps per CTA: 12 (three per SM sub-partition, more warps to hide
 // the LDS -> butterfly -> DMMA latency) where that measured faster — the low
