@@ -468,9 +468,15 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
                     (2 * C::NSMAX + 2 * NW) * 8 + (8 * C::DO + 8 * NT) * 4 + 64,
                 "s_tile must fit the tail's slack");
 
+  // tile / tcols without an integer division (every warp decodes every tile
+  // id it touches: at m = 2 that division was ~13% of the kernel's instructions):
+  // float reciprocal (tile < 2^24, exact to within one) and one correction each way
+  const float inv_tcols = 1.0f / (float)tcols;
   auto tile_geo = [&](int tile) {
     CMTile t;
-    const int ti = tile / tcols;
+    int ti = (int)((float)tile * inv_tcols);
+    ti -= ti * tcols > tile;
+    ti += (ti + 1) * tcols <= tile;
     t.tr0 = (int64_t)ti * TR;
     t.j0 = (int64_t)(tile - ti * tcols) * TJ;
     const int64_t vr = a.ntrows - t.tr0, vc = a.nty - t.j0;

@@ -74,6 +74,7 @@ cudaError_t launch_cellmap(const CellMapArgs& a, cudaStream_t st) {
     if (dev < kDevs) grid_cache[dev].store(cached, std::memory_order_release);
   }
   const int64_t ntiles = ((a.nty + C::TJ - 1) / C::TJ) * ((a.ntrows + C::TR - 1) / C::TR);
+  if (ntiles >= (int64_t(1) << 24)) return cudaErrorInvalidValue;  // the kernel decodes tile ids in float
   int64_t nblk = cached - 1;
   if (nblk > ntiles) nblk = ntiles;
   if (nblk <= 0) return cudaSuccess;
