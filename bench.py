@@ -363,22 +363,33 @@ def slab_run(hb, torch, dist, ring, m, steps, warmup, stream, events=True):
     torch.cuda.synchronize()
     if ring.world > 1:
         dist.barrier()
-    k_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     start = torch.cuda.Event(enable_timing=True)
     stop = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    # the timed region: back-to-back steps, no per-step events (an event record between two
+    # launches would break the programmatic dependent launch that chains them)
     start.record(stream)
     for i in range(steps):
-        ring.kernel_events = k_ev[i] if events else None
         step(warmup + i, parity)
         parity = hb.flip(parity)
     stop.record(stream)
     torch.cuda.synchronize()
-    ring.kernel_events = None
     if ring.world > 1:
         dist.barrier()
     ms = start.elapsed_time(stop)
-    kern_ms = sum(a.elapsed_time(b) for a, b in k_ev) / steps if events else float("nan")
+    # then each step's launch(es) bracketed by events on the launching stream: the kernel's own
+    # average duration (the roofline denominator), PDL overlap excluded
+    kern_ms = float("nan")
+    if events:
+        nk = min(steps, 20)
+        k_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nk)]
+        for i in range(nk):
+            ring.kernel_events = k_ev[i]
+            step(warmup + steps + i, parity)
+            parity = hb.flip(parity)
+        torch.cuda.synchronize()
+        ring.kernel_events = None
+        kern_ms = sum(a.elapsed_time(b) for a, b in k_ev) / nk
     if ring.world > 1:  # the job's time is the slowest rank's
         t = torch.tensor([ms, kern_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
