@@ -4,6 +4,7 @@
 //   tools/cellmap_probe [n]
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "../paper_1802_05246_b200/csrc/cellmap.cuh"
@@ -119,19 +120,21 @@ void probe(int64_t n, bool zeros) {
 
 int main(int argc, char** argv) {
   const int64_t n = argc > 1 ? atoll(argv[1]) : 1024;
+  const char* only = argc > 2 ? argv[2] : nullptr;  // e.g. "d2" (dissipative m = 2) or "c5"
+  auto want = [&](const char* k) { return only == nullptr || strcmp(only, k) == 0; };
   setvbuf(stdout, nullptr, _IOLBF, 0);
   for (int z = 1; z >= 1; --z) {
-    probe<2, kDiss>(n, z);
-    probe<3, kDiss>(n, z);
-    probe<4, kDiss>(n, z);
-    probe<5, kDiss>(n, z);
-    probe<6, kDiss>(n, z);
-    probe<7, kDiss>(n, z);
-    probe<8, kDiss>(n, z);
-    probe<3, kCons>(n, z);
-    probe<4, kCons>(n, z);
-    probe<5, kCons>(n, z);
-    probe<8, kCons>(n, z);
+    if (want("d2")) probe<2, kDiss>(n, z);
+    if (want("d3")) probe<3, kDiss>(n, z);
+    if (want("d4")) probe<4, kDiss>(n, z);
+    if (want("d5")) probe<5, kDiss>(n, z);
+    if (want("d6")) probe<6, kDiss>(n, z);
+    if (want("d7")) probe<7, kDiss>(n, z);
+    if (want("d8")) probe<8, kDiss>(n, z);
+    if (want("c3")) probe<3, kCons>(n, z);
+    if (want("c4")) probe<4, kCons>(n, z);
+    if (want("c5")) probe<5, kCons>(n, z);
+    if (want("c8")) probe<8, kCons>(n, z);
   }
   return 0;
 }
