@@ -935,17 +935,37 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
         const unsigned long long mx = ((kxbits >> step) & 1ull) << 63;
         const unsigned long long my = ((kybits >> step) & 1ull) << 63;
         double A[MT][4];
+        if constexpr (cm_yfirst(SCH, M)) {
+          // y-pairs first, per staged row (row t + 1 is shared by M-tiles t and
+          // t + 1): 2 (MT + 1) + 4 MT additions instead of 8 MT
+          double P[MT + 1], Q[MT + 1];
 #pragma unroll
-        for (int t = 0; t < MT; ++t) {
-          const double c00 = raw[cur][t][0];
-          const double c01 = flip_sign(raw[cur][t][1], my);
-          const double c10 = flip_sign(raw[cur][t + 1][0], mx);
-          const double c11 = flip_sign(raw[cur][t + 1][1], mx ^ my);
-          const double ap = c00 + c10, am = c00 - c10, bp = c01 + c11, bm = c01 - c11;
-          A[t][0] = ap + bp;  // class (0,0)
-          A[t][1] = ap - bp;  // class (0,1)
-          A[t][2] = am + bm;  // class (1,0)
-          A[t][3] = am - bm;  // class (1,1)
+          for (int r = 0; r <= MT; ++r) {
+            const double yl = raw[cur][r][0], yr = flip_sign(raw[cur][r][1], my);
+            P[r] = yl + yr;  // y-even classes
+            Q[r] = yl - yr;  // y-odd classes
+          }
+#pragma unroll
+          for (int t = 0; t < MT; ++t) {
+            const double p1 = flip_sign(P[t + 1], mx), q1 = flip_sign(Q[t + 1], mx);
+            A[t][0] = P[t] + p1;  // class (0,0)
+            A[t][1] = Q[t] + q1;  // class (0,1)
+            A[t][2] = P[t] - p1;  // class (1,0)
+            A[t][3] = Q[t] - q1;  // class (1,1)
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < MT; ++t) {
+            const double c00 = raw[cur][t][0];
+            const double c01 = flip_sign(raw[cur][t][1], my);
+            const double c10 = flip_sign(raw[cur][t + 1][0], mx);
+            const double c11 = flip_sign(raw[cur][t + 1][1], mx ^ my);
+            const double ap = c00 + c10, am = c00 - c10, bp = c01 + c11, bm = c01 - c11;
+            A[t][0] = ap + bp;  // class (0,0)
+            A[t][1] = ap - bp;  // class (0,1)
+            A[t][2] = am + bm;  // class (1,0)
+            A[t][3] = am - bm;  // class (1,1)
+          }
         }
         const double* wk = wb + ks * NTD * 32 + lane;
         if constexpr (LC > 0) {

@@ -92,6 +92,18 @@ constexpr bool cm_prevreg(int sch, int m) {
   return sch == 1 && (m == 5 || m == 6);
 }
 
+// Corner butterfly order: y-pairs per staged row first (shared by the stacked
+// M-tiles: 2 (MT + 1) + 4 MT additions instead of 8 MT) where it measured
+// faster — dissipative m = 3..5 (+0.6% m = 4, +1.3% m = 5); x-pairs first
+// elsewhere (m = 2: 4.5% slower y-first; m = 6..8 ~1%)
+// (profiles/ab_r02_kernel_knobs.txt).
+constexpr bool cm_yfirst(int sch, int m) {
+#ifdef HW_CM_YFIRST
+  if (cm_knob_h(sch, m)) return HW_CM_YFIRST;
+#endif
+  return sch == 0 && m >= 3 && m <= 5;
+}
+
 // Input slots: each field's entries padded to a multiple of 4 (a 4-deep
 // DMMA k-step never straddles the two fields): field 0 in [0, K0), field 1
 // from K0.  k-steps of 4 slots: NK.
