@@ -191,11 +191,13 @@ def test_builtin_exact_matches_callable():
     assert math.isfinite(e_dev)
 
 
+@pytest.mark.parametrize("pinned", [False, True])
 @pytest.mark.parametrize("per,par", [(True, hb.PRIMAL), (True, hb.DUAL), (False, hb.PRIMAL), (False, hb.DUAL)])
-def test_host_pipelined_path_equals_device_path(per, par):
+def test_host_pipelined_path_equals_device_path(per, par, pinned):
     """numpy in/out of >= 64 rows goes through the chunked, copy-overlapped path
-    (stepping._diss2d_host_pipelined); every cell's arithmetic is the same, so
-    it must equal the device-resident path bit for bit."""
+    (stepping._diss2d_host_pipelined; pageable inputs through pinned staging,
+    pinned ones straight); every cell's arithmetic is the same, so it must
+    equal the device-resident path bit for bit."""
     import torch
 
     m, nx, ny = 3, 150, 37
@@ -207,7 +209,9 @@ def test_host_pipelined_path_equals_device_path(per, par):
     u0 = rng.standard_normal(shp + (m + 1, m + 1))
     v0 = rng.standard_normal(shp + (m, m))
     cfg = hb.SchemeConfig(m=m, lam=0.9)
-    a = hb.half_step_2d(hb.FieldPair(hb.Field2D(grid, par, 0.0, u0), hb.Field2D(grid, par, 0.0, v0)), cfg, bc)
+    uh, vh = (torch.from_numpy(u0).pin_memory().numpy(), torch.from_numpy(v0).pin_memory().numpy()) if pinned \
+        else (u0, v0)
+    a = hb.half_step_2d(hb.FieldPair(hb.Field2D(grid, par, 0.0, uh), hb.Field2D(grid, par, 0.0, vh)), cfg, bc)
     b = hb.half_step_2d(hb.FieldPair(hb.Field2D(grid, par, 0.0, torch.from_numpy(u0).cuda()),
                                      hb.Field2D(grid, par, 0.0, torch.from_numpy(v0).cuda())), cfg, bc)
     assert isinstance(a.u.values, np.ndarray) and a.time == b.time and a.parity == b.parity
