@@ -149,7 +149,8 @@ static DevMap device_map(int scheme, int m, double dt, double hx, double hy, dou
   // fragment tiles: DMMA tiles (ntd) then SIMT tiles, whose columns are the
   // left-over outputs of the hybrid classes (cellmap_shape.h)
   const int nk = cm_nk(scheme, m), nt = cm_nt(scheme, m), ntd = cm_ntd(scheme, m), lc = cm_lc(scheme, m);
-  std::vector<double> wf((size_t)nk * ntd * 32, 0.0), wl((size_t)nk * lc * 4, 0.0);
+  const int ntb = cm_ntb(scheme, m);  // B fragments per k-step
+  std::vector<double> wf((size_t)nk * ntb * 32, 0.0), wl((size_t)nk * lc * 4, 0.0);
   std::vector<int> oc((size_t)nt * 8, -1), ic((size_t)nk * 4, 0);
   // input slot -> map input e (field 0 entries, then field 1); -1 = pad slot
   const int p0 = cm.w_in[0] * cm.w_in[0], p1 = cm.w_in[1] * cm.w_in[1], k0 = cm_k0(scheme, m);
@@ -162,8 +163,31 @@ static DevMap device_map(int scheme, int m, double dt, double hx, double hy, dou
     slot_e[sl] = f1 ? p0 + ee : ee;
     ic[sl] = ((ee / w) & 1) | (((ee % w) & 1) << 1);
   }
-  for (int c = 0; c < 4; ++c) {
+  for (int c = 0; c < 4; ++c)
     if (cm.ncls[c] != cm_ncls(scheme, m, c)) throw Error(HW_EINVAL, "internal: class size mismatch");
+  if (cm_pxm(scheme, m)) {
+    // merged x-classes (cellmap_shape.h): tile group PB holds the outputs of
+    // classes (0, PB) then (1, PB); fragment 2 j + dx of k-step ks multiplies
+    // corner row dx's y-pair sums, the lower row's x-sign (-1)^(PA + kx) folded in
+    for (int pb = 0; pb < 2; ++pb) {
+      const int base = pb ? cm_pxm_tiles(scheme, m, 0) : 0, ntile = cm_pxm_tiles(scheme, m, pb);
+      std::vector<std::pair<int, int>> cols;  // (class, output)
+      for (int pa = 0; pa < 2; ++pa)
+        for (int o = 0; o < cm.ncls[2 * pa + pb]; ++o) cols.emplace_back(2 * pa + pb, o);
+      for (size_t j = 0; j < cols.size(); ++j) oc[(size_t)(base + j / 8) * 8 + j % 8] = cm.code[cols[j].first][cols[j].second];
+      for (int ks = 0; ks < nk; ++ks)
+        for (int jt = 0; jt < ntile; ++jt)
+          for (int dx = 0; dx < 2; ++dx)
+            for (int lane = 0; lane < 32; ++lane) {
+              const int col = 8 * jt + lane / 4, sl = 4 * ks + lane % 4, e = slot_e[sl];
+              if (col >= (int)cols.size() || e < 0) continue;
+              const int c = cols[col].first, o = cols[col].second, pa = c >> 1, kx = ic[sl] & 1;
+              const double sg = (dx && ((pa + kx) & 1)) ? -1.0 : 1.0;
+              wf[((size_t)ks * ntb + 2 * (base + jt) + dx) * 32 + lane] = sg * cm.w[c][(size_t)o * cm.din + e];
+            }
+    }
+  }
+  for (int c = 0; c < 4 && !cm_pxm(scheme, m); ++c) {
     const int base = cm_ntbase(scheme, m, c), ntc = cm_ntc(scheme, m, c);
     const int ndm = std::min(cm.ncls[c], 8 * ntc);  // outputs in DMMA tiles; the rest are SIMT columns
     for (int o = 0; o < ndm; ++o) oc[(size_t)(base + o / 8) * 8 + o % 8] = cm.code[c][o];
@@ -171,7 +195,7 @@ static DevMap device_map(int scheme, int m, double dt, double hx, double hy, dou
       for (int j = 0; j < ntc; ++j)
         for (int lane = 0; lane < 32; ++lane) {
           const int o = 8 * j + lane / 4, e = slot_e[4 * ks + lane % 4];
-          if (o < ndm && e >= 0) wf[((size_t)ks * ntd + base + j) * 32 + lane] = cm.w[c][(size_t)o * cm.din + e];
+          if (o < ndm && e >= 0) wf[((size_t)ks * ntb + base + j) * 32 + lane] = cm.w[c][(size_t)o * cm.din + e];
         }
     for (int q = 0; q < cm_left(scheme, m, c); ++q) {
       const int jcol = cm_lbase(scheme, m, c) + q, o = ndm + q;

@@ -41,7 +41,7 @@ namespace hw {
 
 struct CellMapArgs {
   Rows f0, f1;                 // source fields (f1 unused when the scheme has one input)
-  const double* wfrag;         // [NK][NTD][32] B fragments of the DMMA tiles
+  const double* wfrag;         // [NK][NTB][32] B fragments of the DMMA tiles (cellmap_shape.h cm_ntb)
   const double* wleft;         // [NK][LC][4] weights of the SIMT columns (cellmap_shape.h hybrid tiles)
   const int* ocode;            // [NT][8] output field << 16 | offset in its record, -1 = padding
   const int* icode;            // [NK*4] (kx & 1) | (ky & 1) << 1 of each input slot
@@ -116,6 +116,9 @@ struct CMCfg {
   static constexpr int O1 = cm_wout(SCH, M, 1) * cm_wout(SCH, M, 1);
   static constexpr int NK = cm_nk(SCH, M), NT = cm_nt(SCH, M);
   static constexpr int NTD = cm_ntd(SCH, M), LC = cm_lc(SCH, M);  // DMMA tiles; SIMT columns (hybrid tiles)
+  static constexpr bool PXM = cm_pxm(SCH, M);      // merged x-classes (cellmap_shape.h)
+  static constexpr int NTB = cm_ntb(SCH, M);       // B fragments per k-step
+  static constexpr int TG1 = PXM ? cm_pxm_tiles(SCH, M, 0) : 0;  // PXM: first tile of the y-odd classes
   static constexpr int WLN = NK * LC * 4;                          // resident SIMT weights (doubles)
   static constexpr int B1 = cm_ntbase(SCH, M, 1), B2 = cm_ntbase(SCH, M, 2), B3 = cm_ntbase(SCH, M, 3);
   static constexpr int KSC = cm_ksc(SCH, M);       // k-steps per chunk
@@ -154,9 +157,9 @@ struct CMCfg {
   // WRES: all NK k-steps of W stay resident in shared memory (loaded once per
   // CTA) instead of riding in every ring slot (cm_wres: where that measured
   // faster; W <= 40 KB).
-  static constexpr bool WRES = cm_wres(SCH, M) && NK * NTD * 256 <= 40 * 1024;
-  static constexpr int WRESN = WRES ? NK * NTD * 32 : 0;  // doubles
-  static constexpr int sbuf(int mt) { return (NW * mt / (TJ / 8) + 1) * (TJ + 1) * KCP + (WRES ? 0 : KSC * NTD * 32); }
+  static constexpr bool WRES = cm_wres(SCH, M) && NK * NTB * 256 <= 40 * 1024;
+  static constexpr int WRESN = WRES ? NK * NTB * 32 : 0;  // doubles
+  static constexpr int sbuf(int mt) { return (NW * mt / (TJ / 8) + 1) * (TJ + 1) * KCP + (WRES ? 0 : KSC * NTB * 32); }
   // DIRECT: the consumers store their accumulators straight to HBM (no slab,
   // no producer drain).  SELF: each consumer warp drains its own slab
   // (fragment-order stores, record-order coalesced copy-out), no handoff.
@@ -196,7 +199,7 @@ struct CMCfg {
   static constexpr int TR = NW * MT / (TJ / 8);    // target rows per tile
   static constexpr int NODES = (TR + 1) * (TJ + 1);
   static constexpr int CBUF = NODES * KCP;
-  static constexpr int WBUF = WRES ? 0 : KSC * NTD * 32;
+  static constexpr int WBUF = WRES ? 0 : KSC * NTB * 32;
   static constexpr int SBUF = CBUF + WBUF;         // doubles per ring slot
   // bit ch: ring chunk ch lies inside one field whose record length is even
   // (so a multiple of 4: no padding slots) -> 16-byte staging copies
@@ -246,7 +249,7 @@ struct CMCfg {
   static constexpr int SMEM = NS * SBUF * 8 + TAIL;
   // W fragments double-buffered in registers too where NT <= 8, except for the
   // dissipative m <= 4, where reading them at use measured 0.5-0.8% faster
-  static constexpr bool PREFETCH_B0 = NTD <= 8 && !(SCH == kDiss && M <= 4);
+  static constexpr bool PREFETCH_B0 = NTB <= 8 && !(SCH == kDiss && M <= 4);
 #ifdef HW_CM_PREB
   static constexpr bool PREFETCH_B = cm_knob(SCH, M) ? HW_CM_PREB : PREFETCH_B0;
 #else
@@ -784,13 +787,13 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       // W fragments of the chunk (contiguous, 16-byte aligned)
       const int nks = (C::NK - ch * KSC) < KSC ? (C::NK - ch * KSC) : KSC;
       if (!C::WRES) {
-        const double* wsrc = a.wfrag + ch * KSC * C::NTD * 32;
+        const double* wsrc = a.wfrag + ch * KSC * C::NTB * 32;
         double* wb = cb + C::CBUF;
 #pragma unroll 1
-        for (int i = pl; i < nks * C::NTD * 16; i += NPL) cm_cp_async16(wb + 2 * i, wsrc + 2 * i);
+        for (int i = pl; i < nks * C::NTB * 16; i += NPL) cm_cp_async16(wb + 2 * i, wsrc + 2 * i);
       } else if (g == 0) {  // the whole W once; stage 0's cp.async arrive covers it
 #pragma unroll 1
-        for (int i = pl; i < C::NK * C::NTD * 16; i += NPL) cm_cp_async16(smem + C::WRES0 + 2 * i, a.wfrag + 2 * i);
+        for (int i = pl; i < C::NK * C::NTB * 16; i += NPL) cm_cp_async16(smem + C::WRES0 + 2 * i, a.wfrag + 2 * i);
       }
       mbar_arrive(&full[b]);           // orders this lane's plain shared stores
       mbar_arrive_cp_async(&full[b]);  // fires when this lane's copies have landed
@@ -846,7 +849,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
   for (int t = 0; t < MT; ++t)
 #pragma unroll
     for (int n = 0; n < NT; ++n) acc[t][n][0] = acc[t][n][1] = 0.0;
-  constexpr int LC = C::LC, NTD = C::NTD;
+  constexpr int LC = C::LC, NTD = C::NTD, NTB = C::NTB;
   double part[MT][LC > 0 ? LC : 1];  // SIMT columns: this lane's partial sums over its input slots
   double pvr[C::PREVREG ? MT : 1][C::PREVREG ? NT : 1][2];  // PREVREG: `previous` at this lane's accumulator slots
 
@@ -902,7 +905,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
 #endif
     if (ch != 0) mbar_wait(&full[b], (g / NS) & 1);
     const double* cb = smem + b * C::SBUF;
-    const double* wb = C::WRES ? smem + C::WRES0 + ch * KSC * NTD * 32 : cb + C::CBUF;
+    const double* wb = C::WRES ? smem + C::WRES0 + ch * KSC * NTB * 32 : cb + C::CBUF;
     // One chunk of NKS k-steps, software-pipelined: the shared-memory
     // operands of k-step ks+1 (corner values; W fragments when registers
     // allow) are loaded before the DMMAs of k-step ks issue.  FIRST: the
@@ -914,7 +917,7 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
       // raw[.][r] = the two y-corners of staged row trl0 + r (row r + 1 of
       // M-tile r is row 0 of M-tile r + 1: MT + 1 rows feed MT M-tiles)
       double raw[2][MT + 1][2];
-      double bb[PREB ? 2 : 1][NTD];
+      double bb[PREB ? 2 : 1][NTB];
       const int trl0 = (warp / (TJ / 8)) * MT, tc = (warp % (TJ / 8)) * 8;
       const double* pbase = cb + (trl0 * (TJ + 1) + tc + (lane >> 2)) * KCP + (lane & 3);
       auto load = [&](const int ks, const int slot) {
@@ -925,9 +928,9 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
           raw[slot][r][1] = p[KCP];
         }
         if (PREB) {
-          const double* wk = wb + ks * NTD * 32 + lane;
+          const double* wk = wb + ks * NTB * 32 + lane;
 #pragma unroll
-          for (int nt = 0; nt < NTD; ++nt) bb[PREB ? slot : 0][nt] = wk[nt * 32];
+          for (int nt = 0; nt < NTB; ++nt) bb[PREB ? slot : 0][nt] = wk[nt * 32];
         }
       };
       load(0, 0);
@@ -939,6 +942,33 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
         const unsigned long long mx = ((kxbits >> step) & 1ull) << 63;
         const unsigned long long my = ((kybits >> step) & 1ull) << 63;
         double A[MT][4];
+        const double* wk = wb + ks * NTB * 32 + lane;
+        if constexpr (C::PXM) {
+          // y-pair sums per staged row; the tensor cores combine the rows
+          double P[MT + 1], Q[MT + 1];
+#pragma unroll
+          for (int r = 0; r <= MT; ++r) {
+            const double yl = raw[cur][r][0], yr = flip_sign(raw[cur][r][1], my);
+            P[r] = yl + yr;  // y-even classes
+            Q[r] = yl - yr;  // y-odd classes
+          }
+#pragma unroll
+          for (int nt = 0; nt < NTD; ++nt) {
+#pragma unroll
+            for (int dx = 0; dx < 2; ++dx) {
+              const double bf = PREB ? bb[PREB ? cur : 0][2 * nt + dx] : wk[(2 * nt + dx) * 32];
+#pragma unroll
+              for (int t = 0; t < MT; ++t) {
+                const double av = nt < C::TG1 ? P[t + dx] : Q[t + dx];
+                if (FIRST && ks == 0 && dx == 0)
+                  dmma_first(acc[t][nt], av, bf);
+                else
+                  dmma(acc[t][nt], av, bf);
+              }
+            }
+          }
+          continue;
+        }
         if constexpr (cm_yfirst(SCH, M)) {
           // y-pairs first, per staged row (row t + 1 is shared by M-tiles t and
           // t + 1): 2 (MT + 1) + 4 MT additions instead of 8 MT
@@ -971,7 +1001,6 @@ __global__ void __launch_bounds__(CMCfg<M, SCH>::NTHREADS, 1) cellmap_kernel(con
             A[t][3] = am - bm;  // class (1,1)
           }
         }
-        const double* wk = wb + ks * NTD * 32 + lane;
         if constexpr (LC > 0) {
           // SIMT columns: W_c[o][slot] for this lane's slot (4 distinct per warp: one wavefront)
           const double* wl = smem + C::WL0 + step * LC * 4 + (lane & 3);

@@ -52,7 +52,9 @@ constexpr int cm_lmask(int sch, int m) {
   return (sch == 1 && m == 5) ? 0xf : 0;
 }
 constexpr int cm_rem(int sch, int m, int c) { return cm_ncls(sch, m, c) % 8; }
-constexpr int cm_left(int sch, int m, int c) { return (cm_lmask(sch, m) >> c & 1) ? cm_rem(sch, m, c) : 0; }
+constexpr int cm_left(int sch, int m, int c) {
+  return (cm_lmask(sch, m) >> c & 1) && !(sch == 0 && m <= 2) ? cm_rem(sch, m, c) : 0;  // (none under PXM)
+}
 // DMMA n-tiles of class c and their prefix sums
 constexpr int cm_ntc(int sch, int m, int c) {
   return cm_left(sch, m, c) ? cm_ncls(sch, m, c) / 8 : (cm_ncls(sch, m, c) + 7) / 8;
@@ -61,7 +63,28 @@ constexpr int cm_ntbase(int sch, int m, int c) {  // non-recursive: folds inside
   return (c > 0 ? cm_ntc(sch, m, 0) : 0) + (c > 1 ? cm_ntc(sch, m, 1) : 0) + (c > 2 ? cm_ntc(sch, m, 2) : 0) +
          (c > 3 ? cm_ntc(sch, m, 3) : 0);
 }
-constexpr int cm_ntd(int sch, int m) { return cm_ntbase(sch, m, 4); }  // DMMA tiles
+// Merged x-classes (PXM, the dissipative m <= 2): the outputs of classes
+// (0, PB) and (1, PB) share n-tiles, and the x-combination of the corners
+// runs on the tensor cores instead of the butterfly: each tile takes two DMMAs
+// per k-step, one on the upper and one on the lower corner row's y-pair sums
+// (P = U(r,0) + s U(r,1), Q = U(r,0) - s U(r,1); s = (-1)^ky), with the
+// x-signs (-1)^((PA + kx) dx) folded into the W fragments of the lower row.
+// At m = 2 the classes hold 5 / 3 / 3 / 2 outputs, so 4 class tiles become
+// 2 merged tiles x 2 rows (the same DMMA count) while the additions per
+// k-step fall from 8 MT to 2 (MT + 1) — the FP64 datapath DMMA and DADD share.
+constexpr bool cm_pxm(int sch, int m) {
+#ifdef HW_CM_PXM
+  if (cm_knob_h(sch, m)) return HW_CM_PXM && sch == 0 && m <= 2;
+#endif
+  return sch == 0 && m <= 2;
+}
+constexpr int cm_pxm_n(int sch, int m, int pb) { return cm_ncls(sch, m, pb) + cm_ncls(sch, m, 2 + pb); }
+constexpr int cm_pxm_tiles(int sch, int m, int pb) { return (cm_pxm_n(sch, m, pb) + 7) / 8; }
+constexpr int cm_ntd(int sch, int m) {  // DMMA tiles
+  return cm_pxm(sch, m) ? cm_pxm_tiles(sch, m, 0) + cm_pxm_tiles(sch, m, 1) : cm_ntbase(sch, m, 4);
+}
+// B fragments per k-step: one per DMMA tile, two (upper / lower corner row) under PXM
+constexpr int cm_ntb(int sch, int m) { return cm_pxm(sch, m) ? 2 * cm_ntd(sch, m) : cm_ntd(sch, m); }
 // SIMT columns (left-over outputs, class 0's first) and SIMT tiles
 constexpr int cm_lbase(int sch, int m, int c) {
   return (c > 0 ? cm_left(sch, m, 0) : 0) + (c > 1 ? cm_left(sch, m, 1) : 0) + (c > 2 ? cm_left(sch, m, 2) : 0) +
