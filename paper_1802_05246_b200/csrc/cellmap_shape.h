@@ -176,12 +176,13 @@ constexpr int cm_nw(int sch, int m) {
 
 // W resident in shared memory for the whole kernel instead of staged per
 // ring chunk: measured 2-6% faster for diss m = 3, 4 and cons m = 3..5,
-// neutral at diss m = 5, 5% slower at m = 2 (tools/cellmap_probe, round 1).
+// neutral at diss m = 5 (tools/cellmap_probe, round 1); at diss m = 2 5%
+// slower with the four-class tiles, 1.3% faster with the merged ones (round 2).
 constexpr bool cm_wres(int sch, int m) {
 #ifdef HW_CM_WRES
   if (cm_knob(sch, m)) return HW_CM_WRES;
 #endif
-  return sch == 0 ? (m == 3 || m == 4) : (m >= 3 && m <= 5);
+  return sch == 0 ? (m >= 2 && m <= 4) : (m >= 3 && m <= 5);
 }
 
 // Target columns per tile (tile = TR rows x TJ columns; the staged halo is
