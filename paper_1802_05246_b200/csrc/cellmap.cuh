@@ -221,8 +221,9 @@ struct CMCfg {
   // The fragment-order slab rotates n-tile nt's 32 lane slots by SWZ * nt:
   // the drain's record-order gather then spreads a cell's outputs of equal
   // column over more banks (the consumer's 16-byte stores stay conflict-free).
-  // Measured 1.5-4% faster for every order except conservative m = 3 (+4%).
-  static constexpr int SWZ0 = (SCH == kCons && M == 3) ? 0 : 1;
+  // Measured 1.5-4% faster for every order (conservative m = 3: 4% slower with
+  // its four class tiles in round 1, 2.5% faster with the merged ones).
+  static constexpr int SWZ0 = 1;
 #ifdef HW_CM_SWZ
   static constexpr int SWZ = cm_knob(SCH, M) ? HW_CM_SWZ : SWZ0;
 #else

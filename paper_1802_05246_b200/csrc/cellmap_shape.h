@@ -35,6 +35,22 @@ constexpr int cm_ncls(int sch, int m, int c) {
          cm_cnt_par(cm_wout(sch, m, 1), c >> 1) * cm_cnt_par(cm_wout(sch, m, 1), c & 1);
 }
 
+// Merged x-classes (PXM; the dissipative m <= 2, conservative / bootstrap
+// m = 3 — where the merged tiles need no more DMMAs): the outputs of classes
+// (0, PB) and (1, PB) share n-tiles, and the x-combination of the corners
+// runs on the tensor cores instead of the butterfly: each tile takes two DMMAs
+// per k-step, one on the upper and one on the lower corner row's y-pair sums
+// (P = U(r,0) + s U(r,1), Q = U(r,0) - s U(r,1); s = (-1)^ky), with the
+// x-signs (-1)^((PA + kx) dx) folded into the W fragments of the lower row.
+// At m = 2 the classes hold 5 / 3 / 3 / 2 outputs, so 4 class tiles become
+// 2 merged tiles x 2 rows (the same DMMA count) while the additions per
+// k-step fall from 8 MT to 2 (MT + 1) — the FP64 datapath DMMA and DADD share.
+constexpr bool cm_pxm(int sch, int m) {
+#ifdef HW_CM_PXM
+  if (cm_knob_h(sch, m)) return HW_CM_PXM && (sch == 0 ? m <= 2 : m == 3);
+#endif
+  return sch == 0 ? m <= 2 : m == 3;
+}
 // Hybrid tiles.  A class's outputs fill 8-wide DMMA n-tiles (m8n8k4: N = 8);
 // where class c's remainder r_c = n_c mod 8 is in the class mask cm_lmask,
 // those r_c outputs are computed on the CUDA cores instead of padding a
@@ -53,7 +69,7 @@ constexpr int cm_lmask(int sch, int m) {
 }
 constexpr int cm_rem(int sch, int m, int c) { return cm_ncls(sch, m, c) % 8; }
 constexpr int cm_left(int sch, int m, int c) {
-  return (cm_lmask(sch, m) >> c & 1) && !(sch == 0 && m <= 2) ? cm_rem(sch, m, c) : 0;  // (none under PXM)
+  return (cm_lmask(sch, m) >> c & 1) && !cm_pxm(sch, m) ? cm_rem(sch, m, c) : 0;  // (none under PXM)
 }
 // DMMA n-tiles of class c and their prefix sums
 constexpr int cm_ntc(int sch, int m, int c) {
@@ -62,21 +78,6 @@ constexpr int cm_ntc(int sch, int m, int c) {
 constexpr int cm_ntbase(int sch, int m, int c) {  // non-recursive: folds inside unrolled device loops
   return (c > 0 ? cm_ntc(sch, m, 0) : 0) + (c > 1 ? cm_ntc(sch, m, 1) : 0) + (c > 2 ? cm_ntc(sch, m, 2) : 0) +
          (c > 3 ? cm_ntc(sch, m, 3) : 0);
-}
-// Merged x-classes (PXM, the dissipative m <= 2): the outputs of classes
-// (0, PB) and (1, PB) share n-tiles, and the x-combination of the corners
-// runs on the tensor cores instead of the butterfly: each tile takes two DMMAs
-// per k-step, one on the upper and one on the lower corner row's y-pair sums
-// (P = U(r,0) + s U(r,1), Q = U(r,0) - s U(r,1); s = (-1)^ky), with the
-// x-signs (-1)^((PA + kx) dx) folded into the W fragments of the lower row.
-// At m = 2 the classes hold 5 / 3 / 3 / 2 outputs, so 4 class tiles become
-// 2 merged tiles x 2 rows (the same DMMA count) while the additions per
-// k-step fall from 8 MT to 2 (MT + 1) — the FP64 datapath DMMA and DADD share.
-constexpr bool cm_pxm(int sch, int m) {
-#ifdef HW_CM_PXM
-  if (cm_knob_h(sch, m)) return HW_CM_PXM && sch == 0 && m <= 2;
-#endif
-  return sch == 0 && m <= 2;
 }
 constexpr int cm_pxm_n(int sch, int m, int pb) { return cm_ncls(sch, m, pb) + cm_ncls(sch, m, 2 + pb); }
 constexpr int cm_pxm_tiles(int sch, int m, int pb) { return (cm_pxm_n(sch, m, pb) + 7) / 8; }
