@@ -194,7 +194,8 @@ constexpr int cm_tj(int sch, int m) {
 #ifdef HW_CM_TJ
   if (cm_knob(sch, m)) return HW_CM_TJ;
 #endif
-  return (sch == 0 && m == 4) || (sch != 0 && (m == 4 || m == 8)) ? 16 : 32;
+  // (diss m = 3, round 2: 16 columns, whose smaller ring slots give a 4-deep ring, 6-9% faster)
+  return (sch == 0 && (m == 3 || m == 4)) || (sch != 0 && (m == 4 || m == 8)) ? 16 : 32;
 }
 
 // Epilogue straight from the accumulators to HBM (no slab, no producer
