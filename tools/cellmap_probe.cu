@@ -45,22 +45,24 @@ void probe(int64_t n, bool zeros) {
   using C = CMCfg<M, SCH>;
   CellMapArgs a;
   memset(&a, 0, sizeof(a));
-  double *f0, *f1, *o0, *o1, *w;
+  double *f0, *f1, *o0, *o1, *w, *wl;
   int *oc, *ic;
   cudaMalloc(&f0, n * n * C::P0 * 8);
   cudaMalloc(&f1, n * n * (C::P1 ? C::P1 : 1) * 8);
   cudaMalloc(&o0, n * n * C::O0 * 8);
   cudaMalloc(&o1, n * n * (C::O1 ? C::O1 : 1) * 8);
-  cudaMalloc(&w, C::NK * C::NT * 32 * 8);
+  cudaMalloc(&w, C::NK * C::NTB * 32 * 8);
+  cudaMalloc(&wl, (C::WLN > 0 ? C::WLN : 1) * 8);  // hybrid-tile SIMT weights
+  cudaMemset(wl, 0, (C::WLN > 0 ? C::WLN : 1) * 8);
   cudaMalloc(&oc, C::NT * 8 * 4);
   cudaMalloc(&ic, C::NK * 4 * 4);
   cudaMemset(f0, 0, n * n * C::P0 * 8);
   cudaMemset(f1, 0, n * n * (C::P1 ? C::P1 : 1) * 8);
-  cudaMemset(w, 0, C::NK * C::NT * 32 * 8);
+  cudaMemset(w, 0, C::NK * C::NTB * 32 * 8);
   if (!zeros) {
     fill<<<1184, 256>>>(f0, n * n * C::P0, 1.0);
     if (C::P1) fill<<<1184, 256>>>(f1, n * n * C::P1, 1.0);
-    fill<<<64, 256>>>(w, C::NK * C::NT * 32, 0.1);
+    fill<<<64, 256>>>(w, C::NK * C::NTB * 32, 0.1);
   }
   std::vector<int> h(C::NT * 8);
   for (int i = 0; i < C::NT * 8; ++i) {  // cover every output of both fields (the drain's inverse map)
@@ -72,6 +74,7 @@ void probe(int64_t n, bool zeros) {
   a.f0 = {f0, nullptr, nullptr, 0, n};
   a.f1 = {f1, nullptr, nullptr, 0, n};
   a.wfrag = w;
+  a.wleft = wl;
   a.ocode = oc;
   a.icode = ic;
   a.prev = o0;
@@ -115,7 +118,7 @@ void probe(int64_t n, bool zeros) {
   printf("{\"zeros\": %d, \"m\": %d, \"scheme\": %d, \"n\": %ld, \"full_ms\": %.4f, \"loop20_alt_parity_ms\": %.4f, \"no_staging_ms\": %.4f, \"staging_only_ms\": %.4f, \"no_hbm_stores_ms\": %.4f, "
          "\"err\": \"%s\"}\n",
          (int)zeros, M, SCH, (long)n, t0, tloop, t1, t2, t3, cudaGetErrorString(cudaDeviceSynchronize()));
-  cudaFree(f0); cudaFree(f1); cudaFree(o0); cudaFree(o1); cudaFree(w); cudaFree(oc); cudaFree(ic);
+  cudaFree(f0); cudaFree(f1); cudaFree(o0); cudaFree(o1); cudaFree(w); cudaFree(wl); cudaFree(oc); cudaFree(ic);
 }
 
 int main(int argc, char** argv) {
