@@ -64,8 +64,11 @@ constexpr int cm_lmask(int sch, int m) {
 #ifdef HW_CM_LMASK
   if (cm_knob_h(sch, m)) return HW_CM_LMASK;
 #endif
-  // measured (profiles/ab_r02_kernel_knobs.txt): cons m = 5 (+7%); diss m = 4 -2% (0x6) / -7% (0xf): off
-  return (sch == 1 && m == 5) ? 0xf : 0;
+  // measured (profiles/ab_r02_kernel_knobs.txt): cons m = 5 (+7%); one left-over output of class (0,0) on
+  // the CUDA cores in place of a whole n-tile at diss m = 6, 8 (+2.6%, +2.7%) and cons m = 8 (+1%);
+  // off elsewhere (diss m = 4 -2% (0x6) / -7% (0xf), m = 2 20-39% slower, cons m = 4 0x1 -8%)
+  if (sch == 1 && m == 5) return 0xf;
+  return ((sch == 0 && (m == 6 || m == 8)) || (sch == 1 && m == 8)) ? 0x1 : 0;
 }
 constexpr int cm_rem(int sch, int m, int c) { return cm_ncls(sch, m, c) % 8; }
 constexpr int cm_left(int sch, int m, int c) {
