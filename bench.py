@@ -70,7 +70,8 @@ def dof_per_node(m: int, scheme: str = "diss") -> int:
     return (m + 1) ** 2 + m * m if scheme == "diss" else (m + 1) ** 2
 
 
-HYBRID_MASK = {("cons", 5): 0xF}  # csrc/cellmap_shape.h cm_lmask: classes whose left-over outputs run on CUDA cores
+# csrc/cellmap_shape.h cm_lmask: classes whose left-over outputs run on CUDA cores
+HYBRID_MASK = {("cons", 5): 0xF, ("diss", 6): 0x1, ("diss", 8): 0x1, ("cons", 8): 0x1}
 
 
 def cellmap_flops(m: int, scheme: str = "diss"):
