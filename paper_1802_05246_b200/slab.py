@@ -96,7 +96,10 @@ class SlabRing:
         side, send_row, to, frm = self.halo_plan(parity_src)
         if side is None:
             return None, [None] * len(fields), []
-        ops, bufs = [], []
+        # gloo moves host tensors only: CUDA rows are staged through host memory
+        # there (the multi-process GPU test); NCCL sends device rows directly
+        staged = dist.get_backend() == "gloo" and any(f.is_cuda for f in fields)
+        ops, bufs, landed = [], [], []
         for k, f in enumerate(fields):
             buf = None
             if frm is not None:
@@ -105,11 +108,19 @@ class SlabRing:
                 if buf is None:
                     buf = torch.empty(f.shape[1:], dtype=f.dtype, device=f.device)
                     self._halo[key] = buf
-                ops.append(dist.P2POp(dist.irecv, buf, frm))
+                if staged:
+                    hbuf = torch.empty(buf.shape, dtype=buf.dtype)
+                    landed.append((hbuf, buf))
+                    ops.append(dist.P2POp(dist.irecv, hbuf, frm))
+                else:
+                    ops.append(dist.P2POp(dist.irecv, buf, frm))
             if to is not None:
-                ops.append(dist.P2POp(dist.isend, f[send_row].contiguous(), to))
+                row = f[send_row].contiguous()
+                ops.append(dist.P2POp(dist.isend, row.cpu() if staged else row, to))
             bufs.append(buf)
         works = dist.batch_isend_irecv(ops) if ops else []
+        if staged and works:
+            works = [_StagedRecv(works, landed)]
         return side, bufs, works
 
     def _halos(self, side, bufs):
@@ -164,7 +175,8 @@ class SlabRing:
 
         if self.world == 1:
             return list(vals)
-        t = torch.tensor(vals, dtype=torch.float64, device=self.backend.reduce_device())
+        dev = self.backend.reduce_device() if dist.get_backend() != "gloo" else "cpu"
+        t = torch.tensor(vals, dtype=torch.float64, device=dev)
         dist.all_reduce(t)
         return [float(x) for x in t.cpu()]
 
@@ -203,6 +215,20 @@ class SlabRing:
             parts[2] += self.backend.inner(self, cur, tb2, ha[0], ha[1], pa, bc, (m, m), dx, dy, npts, ta0, nta)
         ia, ib, iab = self._allreduce(parts)
         return 2.0 * (ia + ib - iab)
+
+
+class _StagedRecv:
+    """gloo receives of device halos: wait, then copy the host rows to their
+    device buffers (on the current stream, ahead of the edge-row launch)."""
+
+    def __init__(self, works, landed):
+        self.works, self.landed = works, landed
+
+    def wait(self):
+        for w in self.works:
+            w.wait()
+        for host, dev in self.landed:
+            dev.copy_(host, non_blocking=False)
 
 
 class CabiBackend:
