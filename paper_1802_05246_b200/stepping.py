@@ -73,8 +73,10 @@ def _diss2d_host_pipelined(uh, vh, grid, parity, m, cfg: SchemeConfig, bc: Bound
     wall mirror included) have landed, and its results come back on a third
     stream while the next chunk computes.  Same arithmetic as the one-shot
     path (the kernel takes a target-row window, hw_geom2d.trow0/ntrows).
+    Pageable inputs are staged chunk by chunk through pinned buffers.
     `_marks` (tools/e2e_timeline.py): a list that receives (label, timing
-    event) pairs for every upload, kernel and download."""
+    event) pairs for every upload, kernel and download; `_interleave` /
+    `_pinned` override the launch order / input kind (tools/e2e_order.py)."""
     import torch
 
     timing = _marks is not None
