@@ -45,7 +45,7 @@ def _views(g, rings, parity):
     return [g[r.row0: r.row0 + r.nrows(parity)] for r in rings]
 
 
-@pytest.mark.parametrize("m,world", [(3, 2), (4, 4), (6, 2), (6, 4)])
+@pytest.mark.parametrize("m,world", [(1, 4), (2, 2), (3, 2), (4, 4), (6, 2), (6, 4)])
 def test_slab_ranks_equal_whole_grid_bitwise(m, world):
     import paper_1802_05246_b200 as hb
     from paper_1802_05246_b200.stepping import diss2d_into
