@@ -36,7 +36,7 @@ constexpr int cm_ncls(int sch, int m, int c) {
 }
 
 // Merged x-classes (PXM; the dissipative m <= 2, conservative / bootstrap
-// m = 3 — where the merged tiles need no more DMMAs): the outputs of classes
+// m = 3, bootstrap m <= 2 — where the merged tiles need no more DMMAs): the outputs of classes
 // (0, PB) and (1, PB) share n-tiles, and the x-combination of the corners
 // runs on the tensor cores instead of the butterfly: each tile takes two DMMAs
 // per k-step, one on the upper and one on the lower corner row's y-pair sums
@@ -47,9 +47,10 @@ constexpr int cm_ncls(int sch, int m, int c) {
 // k-step fall from 8 MT to 2 (MT + 1) — the FP64 datapath DMMA and DADD share.
 constexpr bool cm_pxm(int sch, int m) {
 #ifdef HW_CM_PXM
-  if (cm_knob_h(sch, m)) return HW_CM_PXM && (sch == 0 ? m <= 2 : m == 3);
+  if (cm_knob_h(sch, m)) return HW_CM_PXM && (sch == 0 ? m <= 2 : (m == 3 || (sch == 2 && m <= 2)));
 #endif
-  return sch == 0 ? m <= 2 : m == 3;
+  // (the conservative m <= 2 runs on the SIMT kernel; the bootstrap m <= 2 on this one)
+  return sch == 0 ? m <= 2 : (m == 3 || (sch == 2 && m <= 2));
 }
 // Hybrid tiles.  A class's outputs fill 8-wide DMMA n-tiles (m8n8k4: N = 8);
 // where class c's remainder r_c = n_c mod 8 is in the class mask cm_lmask,
